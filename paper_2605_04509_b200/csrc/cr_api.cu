@@ -1,0 +1,824 @@
+// cr_api.cu — C ABI (include/coherent_raster.h) and stage orchestration of
+// the CoherentRaster B200 path.  Unity build: includes every kernel header so
+// the __constant__ rig is shared without relocatable device code.
+//
+// Per-frame launch sequence (one stream):
+//   preprocess<DEG>           a4 (+a6 count)           HBM/ALU
+//   scan(cnt>0) -> compact    visible (i,k) records    HBM
+//   radix x4 (depth) + x1 (k) a7 depth presort          HBM
+//   scan(counts)              pair offsets, P          HBM
+//   emit                      a6 <tile, r> pairs        ALU
+//   radix x2..3 (tile)        a7 stable tile sort       HBM
+//   ranges                    a8                        HBM
+//   composite                 a9                        ALU/MUFU
+// Host<->device: two 4-byte reads (visible-record count, P) size the sorts.
+#include <cuda_runtime.h>
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/coherent_raster.h"
+#include "cr_composite.cuh"
+#include "cr_device.cuh"
+#include "cr_kernels.cuh"
+#include "cr_sort.cuh"
+
+#ifndef CR_GIT_TAG
+#define CR_GIT_TAG "dev"
+#endif
+
+namespace {
+
+using namespace cr;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Scan {  // functors for the generic device scan
+  struct InFlag {
+    const uint32_t* cnt;
+    __device__ uint32_t operator()(long long i) const { return cnt[i] > 0u ? 1u : 0u; }
+  };
+  struct OutCompact {
+    const uint32_t* dkey;
+    uint32_t* ko;
+    uint32_t* vo;
+    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
+      if (v) { ko[ex] = dkey[i]; vo[ex] = (uint32_t)i; }
+    }
+  };
+  struct InGather {
+    const uint32_t* cnt;
+    const uint32_t* idx;
+    __device__ uint32_t operator()(long long i) const { return cnt[idx[i]]; }
+  };
+  struct InArr {
+    const uint32_t* a;
+    __device__ uint32_t operator()(long long i) const { return a[i]; }
+  };
+  struct OutStore {
+    uint32_t* o;
+    __device__ void operator()(long long i, uint32_t ex, uint32_t) const { o[i] = ex; }
+  };
+};
+
+}  // namespace
+
+struct cr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // scene
+  bool has_scene = false;
+  long long M = 0;
+  int deg = 0;
+  DevBuf mean4, cov8, shsoa;
+  // display
+  bool has_display = false;
+  cr_display disp{};
+  int TX = 0, TY = 0;
+  DevBuf V, psi;
+  int chunks_s = -1, chunk_stride = 0;
+  DevBuf chunks, nchunks;
+  // rig
+  bool has_rig = false;
+  std::vector<CamDev> cams;
+  std::vector<CamConstDev> ccon;
+  float znear = 0.01f;
+  // frame buffers
+  DevBuf rec0, rec1, cnt, dkey, offs;
+  DevBuf ka, va, kb, vb;           // record sort ping-pong
+  DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
+  DevBuf bsum, hist, scalars, S, E, stage_out;
+  DevBuf tmp;                      // upload staging
+  uint32_t* h_pinned = nullptr;    // small pinned readback
+  // last frame
+  int K = 0, bitK = 1;
+  uint32_t P = 0, nvis = 0;
+  const uint32_t* final_t = nullptr;
+  const uint32_t* final_v = nullptr;
+  bool has_frame = false;
+  int launches = 0;
+  cudaEvent_t ev[6] = {};
+  long long device_bytes = 0;
+  bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
+};
+
+namespace {
+
+cr_status fail(cr_ctx* c, cr_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CR_CUDA(c, call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((c), e_ == cudaErrorMemoryAllocation ? CR_ERR_OUT_OF_MEMORY : CR_ERR_CUDA, \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);     \
+  } while (0)
+
+#define CR_LAUNCHED(c)                                                                     \
+  do {                                                                                     \
+    ++(c)->launches;                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail((c), CR_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+// CR_DEBUG tracing: synchronise the stream and report the stage + CUDA state.
+#define CR_TRACE(c, what)                                                                   \
+  do {                                                                                      \
+    if ((c)->debug) {                                                                       \
+      cudaError_t e_ = cudaStreamSynchronize((c)->stream);                                  \
+      fprintf(stderr, "[cr] %-28s %s\n", what, cudaGetErrorString(e_));                    \
+      fflush(stderr);                                                                       \
+      if (e_ != cudaSuccess) return fail((c), CR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e_)); \
+    }                                                                                       \
+  } while (0)
+
+void segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  fprintf(stderr, "[cr] fatal signal %d, native backtrace:\n", sig);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+
+#define CR_TRY(x)                 \
+  do {                            \
+    cr_status s_ = (x);           \
+    if (s_ != CR_OK) return s_;   \
+  } while (0)
+
+cr_status ensure(cr_ctx* c, DevBuf& b, size_t bytes) {
+  if (bytes <= b.bytes && b.p) return CR_OK;
+  if (b.p) {
+    cudaFree(b.p);
+    c->device_bytes -= (long long)b.bytes;
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return fail(c, CR_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu): %s", want, cudaGetErrorString(e));
+  }
+  b.bytes = want;
+  c->device_bytes += (long long)want;
+  return CR_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+template <class T>
+T* P_(DevBuf& b) { return (T*)b.p; }
+
+unsigned grid_for(long long n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// device exclusive scan: out(i, excl, in(i)); *d_total = sum
+template <class In, class Out>
+cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
+  if (n <= 0) {
+    CR_CUDA(c, cudaMemsetAsync(d_total, 0, 4, c->stream));
+    return CR_OK;
+  }
+  const long long nb = (n + kScanTile - 1) / kScanTile;
+  CR_TRY(ensure(c, c->bsum, (size_t)nb * 4));
+  uint32_t* bs = P_<uint32_t>(c->bsum);
+  k_scan_reduce<In><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, n, bs);
+  CR_LAUNCHED(c);
+  int* ovf = P_<int>(c->scalars) + 3;
+  k_scan_bsums<<<1, 1024, 0, c->stream>>>(bs, (int)nb, d_total, ovf);
+  CR_LAUNCHED(c);
+  k_scan_down<In, Out><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, out, n, bs);
+  CR_LAUNCHED(c);
+  return CR_OK;
+}
+
+// one stable LSD pass
+cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
+                     uint32_t* vout, long long n, int shift, bool from_val,
+                     unsigned long long div, bool move_keys) {
+  if (n <= 0) return CR_OK;
+  const long long nb = (n + kSortTile - 1) / kSortTile;
+  CR_TRY(ensure(c, c->hist, (size_t)nb * 256 * 4));
+  uint32_t* h = P_<uint32_t>(c->hist);
+  if (from_val)
+    k_radix_upsweep<true><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift, div,
+                                                                        h, (int)nb);
+  else
+    k_radix_upsweep<false><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift, div,
+                                                                         h, (int)nb);
+  CR_LAUNCHED(c);
+  uint32_t* tot = P_<uint32_t>(c->scalars) + 2;
+  CR_TRY(dev_scan(c, Scan::InArr{h}, Scan::OutStore{h}, nb * 256, tot));
+  if (from_val && move_keys)
+    k_radix_downsweep<true, true><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+        kin, vin, kout, vout, n, shift, div, h, (int)nb);
+  else if (from_val)
+    k_radix_downsweep<true, false><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+        kin, vin, kout, vout, n, shift, div, h, (int)nb);
+  else
+    k_radix_downsweep<false, true><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+        kin, vin, kout, vout, n, shift, div, h, (int)nb);
+  CR_LAUNCHED(c);
+  return CR_OK;
+}
+
+cr_status read_u32(cr_ctx* c, const uint32_t* d, uint32_t* h) {
+  CR_CUDA(c, cudaMemcpyAsync(c->h_pinned, d, 4, cudaMemcpyDeviceToHost, c->stream));
+  CR_CUDA(c, cudaStreamSynchronize(c->stream));
+  *h = c->h_pinned[0];
+  return CR_OK;
+}
+
+void cam_consts_host(const cr_camera& in, int W, int H, CamDev* d, CamConstDev* k) {
+  std::memcpy(d->R, in.R, sizeof(float) * 9);
+  std::memcpy(d->t, in.t, sizeof(float) * 3);
+  d->fx = in.fx; d->fy = in.fy; d->cx = in.cx; d->cy = in.cy;
+  // O6 frustum clamp constants and O11 camera centre, fp64 -> fp32
+  const double tfx = 0.5 * (double)W / (double)in.fx;
+  const double tfy = 0.5 * (double)H / (double)in.fy;
+  k->limxp = (float)(((double)W - (double)in.cx) / (double)in.fx + 0.3 * tfx);
+  k->limxn = (float)((double)in.cx / (double)in.fx + 0.3 * tfx);
+  k->limyp = (float)(((double)H - (double)in.cy) / (double)in.fy + 0.3 * tfy);
+  k->limyn = (float)((double)in.cy / (double)in.fy + 0.3 * tfy);
+  for (int a = 0; a < 3; ++a) {
+    double v = 0.0;
+    for (int r = 0; r < 3; ++r) v += (double)in.R[r * 3 + a] * (double)in.t[r];
+    k->C[a] = (float)(-v);
+  }
+  k->pad = 0.f;
+}
+
+bool finite_all(const float* p, long long n) {
+  for (long long q = 0; q < n; ++q)
+    if (!std::isfinite(p[q])) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cr_version(void) { return "coherent_raster sm_100a " CR_GIT_TAG; }
+
+const char* cr_status_string(cr_status s) {
+  switch (s) {
+    case CR_OK: return "CR_OK";
+    case CR_ERR_INVALID_ARG: return "CR_ERR_INVALID_ARG";
+    case CR_ERR_INVALID_CONFIG: return "CR_ERR_INVALID_CONFIG";
+    case CR_ERR_CONFIG_MISMATCH: return "CR_ERR_CONFIG_MISMATCH";
+    case CR_ERR_TILE_ID_OVERFLOW: return "CR_ERR_TILE_ID_OVERFLOW";
+    case CR_ERR_NONFINITE: return "CR_ERR_NONFINITE";
+    case CR_ERR_NOT_READY: return "CR_ERR_NOT_READY";
+    case CR_ERR_OUT_OF_MEMORY: return "CR_ERR_OUT_OF_MEMORY";
+    case CR_ERR_CUDA: return "CR_ERR_CUDA";
+    case CR_ERR_CAPACITY: return "CR_ERR_CAPACITY";
+  }
+  return "CR_ERR_UNKNOWN";
+}
+
+cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
+  if (!out) return CR_ERR_INVALID_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device < 0 || cuda_device >= n) {
+    cudaGetLastError();
+    return CR_ERR_CUDA;
+  }
+  cr_ctx* c = new cr_ctx();
+  c->device = cuda_device;
+  const char* dbg = getenv("CR_DEBUG");
+  c->debug = dbg && dbg[0] && dbg[0] != '0';
+  if (c->debug) {
+    signal(SIGSEGV, segv_handler);
+    signal(SIGBUS, segv_handler);
+  }
+  c->stream = (cudaStream_t)cuda_stream;
+  if (cudaSetDevice(cuda_device) != cudaSuccess || cudaMallocHost(&c->h_pinned, 64) != cudaSuccess) {
+    delete c;
+    return CR_ERR_CUDA;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  if (ensure(c, c->scalars, 64) != CR_OK) {
+    delete c;
+    return CR_ERR_OUT_OF_MEMORY;
+  }
+  *out = c;
+  return CR_OK;
+}
+
+void cr_destroy(cr_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
+                   &c->rec0, &c->rec1, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
+                   &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist,
+                   &c->scalars, &c->S, &c->E, &c->stage_out, &c->tmp};
+  for (DevBuf* b : all) release(*b);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  delete c;
+}
+
+cr_status cr_set_stream(cr_ctx* c, void* s) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  c->stream = (cudaStream_t)s;
+  return CR_OK;
+}
+
+const char* cr_last_error(const cr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+cr_status cr_upload_gaussians(cr_ctx* c, int64_t M, int deg, const float* means,
+                              const float* quats, const float* scales, const float* opac,
+                              const float* sh, int on_dev) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  if (M < 0 || deg < 0 || deg > 3) return fail(c, CR_ERR_INVALID_ARG, "M=%lld deg=%d", (long long)M, deg);
+  if (M > 0 && (!means || !quats || !scales || !opac || !sh))
+    return fail(c, CR_ERR_INVALID_ARG, "null Gaussian pointer");
+  if (M > (1LL << 30)) return fail(c, CR_ERR_INVALID_ARG, "M too large");
+  cudaSetDevice(c->device);
+  const int nc3 = (deg + 1) * (deg + 1) * 3;
+  c->has_frame = false;
+  if (M == 0) {
+    c->M = 0;
+    c->deg = deg;
+    c->has_scene = true;
+    return CR_OK;
+  }
+  // tau_i = 2 ln(255 o_i) on the host in fp64 (O4); opacities needed on the host
+  std::vector<float> h_op((size_t)M), h_tau((size_t)M);
+  if (on_dev) {
+    CR_CUDA(c, cudaMemcpyAsync(h_op.data(), opac, 4 * M, cudaMemcpyDeviceToHost, c->stream));
+    CR_CUDA(c, cudaStreamSynchronize(c->stream));
+  } else {
+    std::memcpy(h_op.data(), opac, 4 * M);
+  }
+  for (long long i = 0; i < M; ++i) {
+    if (!std::isfinite(h_op[i])) return fail(c, CR_ERR_NONFINITE, "opacity %lld not finite", i);
+    h_tau[i] = (float)(2.0 * std::log(255.0 * (double)h_op[i]));
+  }
+  const size_t nin = (size_t)M * (3 + 4 + 3 + 1 + 1 + nc3);
+  CR_TRY(ensure(c, c->tmp, nin * 4));
+  float* t = P_<float>(c->tmp);
+  float *d_means = t, *d_quats = d_means + 3 * M, *d_scales = d_quats + 4 * M,
+        *d_op = d_scales + 3 * M, *d_tau = d_op + M, *d_sh = d_tau + M;
+  const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CR_CUDA(c, cudaMemcpyAsync(d_means, means, 12 * M, kind, c->stream));
+  CR_CUDA(c, cudaMemcpyAsync(d_quats, quats, 16 * M, kind, c->stream));
+  CR_CUDA(c, cudaMemcpyAsync(d_scales, scales, 12 * M, kind, c->stream));
+  CR_CUDA(c, cudaMemcpyAsync(d_op, h_op.data(), 4 * M, cudaMemcpyHostToDevice, c->stream));
+  CR_CUDA(c, cudaMemcpyAsync(d_tau, h_tau.data(), 4 * M, cudaMemcpyHostToDevice, c->stream));
+  CR_CUDA(c, cudaMemcpyAsync(d_sh, sh, 4 * (size_t)M * nc3, kind, c->stream));
+  CR_TRY(ensure(c, c->mean4, 16 * (size_t)M));
+  CR_TRY(ensure(c, c->cov8, 32 * (size_t)M));
+  CR_TRY(ensure(c, c->shsoa, 4 * (size_t)M * nc3));
+  int* flag = P_<int>(c->scalars) + 4;
+  CR_CUDA(c, cudaMemsetAsync(flag, 0, 4, c->stream));
+  k_upload<<<grid_for(M, 256), 256, 0, c->stream>>>(M, nc3, d_means, d_quats, d_scales, d_op,
+                                                     d_tau, d_sh, P_<float4>(c->mean4),
+                                                     P_<float4>(c->cov8), P_<float>(c->shsoa),
+                                                     flag);
+  CR_LAUNCHED(c);
+  uint32_t bad = 0;
+  CR_TRY(read_u32(c, (const uint32_t*)flag, &bad));
+  if (bad) {
+    c->has_scene = false;
+    return fail(c, CR_ERR_NONFINITE, "NaN/Inf in uploaded Gaussians");
+  }
+  c->M = M;
+  c->deg = deg;
+  c->has_scene = true;
+  return CR_OK;
+}
+
+cr_status cr_set_display(cr_ctx* c, const cr_display* d) {
+  if (!c || !d) return CR_ERR_INVALID_ARG;
+  const int ts = d->tile_size == 0 ? 16 : d->tile_size;
+  if (d->width < 1 || d->height < 1 || d->num_views < 1 || d->num_views > kMaxViews ||
+      !(d->lens_pitch > 0) || !std::isfinite(d->lens_pitch) || !std::isfinite(d->slant) ||
+      !std::isfinite(d->center_offset) || ts != 16 || d->width > 65535 || d->height > 65535)
+    return fail(c, CR_ERR_INVALID_CONFIG, "invalid display (W=%d H=%d N=%d Lx=%g tile=%d)",
+                d->width, d->height, d->num_views, d->lens_pitch, ts);
+  cudaSetDevice(c->device);
+  const int W = d->width, H = d->height;
+  const int TX = (W + 15) / 16, TY = (H + 15) / 16;
+  CR_TRY(ensure(c, c->V, (size_t)W * H * 3));
+  CR_TRY(ensure(c, c->psi, (size_t)TX * TY * kTileSub * 2));
+  const double tA = std::tan(d->slant);  // Z2: tan on the host in fp64
+  const long long nsub = (long long)W * H * 3;
+  k_viewmap<<<(unsigned)std::min<long long>(grid_for(nsub, 256), 148 * 64), 256, 0, c->stream>>>(
+      P_<uint8_t>(c->V), W, H, d->num_views, d->lens_pitch, tA, d->center_offset);
+  CR_LAUNCHED(c);
+  k_remap_build<<<grid_for((long long)TX * TY, 8), 256, 0, c->stream>>>(
+      P_<uint8_t>(c->V), P_<uint16_t>(c->psi), W, H, TX, TY);
+  CR_LAUNCHED(c);
+  c->disp = *d;
+  c->disp.tile_size = 16;
+  c->TX = TX;
+  c->TY = TY;
+  c->chunks_s = -1;
+  c->has_frame = false;
+  c->has_display = true;
+  if (c->has_rig && (int)c->cams.size() != d->num_views) c->has_rig = false;
+  return CR_OK;
+}
+
+cr_status cr_set_camera_rig(cr_ctx* c, int32_t n, const cr_camera* views, float znear) {
+  if (!c || !views || n < 1) return CR_ERR_INVALID_ARG;
+  if (!c->has_display) return fail(c, CR_ERR_NOT_READY, "set the display before the rig");
+  if (n != c->disp.num_views)
+    return fail(c, CR_ERR_CONFIG_MISMATCH, "rig has %d views, display has %d", n,
+                c->disp.num_views);
+  if (!(znear > 0) || !std::isfinite(znear)) return fail(c, CR_ERR_INVALID_ARG, "znear");
+  for (int j = 0; j < n; ++j)
+    if (!finite_all((const float*)&views[j], 16) || !(views[j].fx > 0) || !(views[j].fy > 0))
+      return fail(c, CR_ERR_NONFINITE, "camera %d not finite / non-positive focal", j);
+  c->cams.resize(n);
+  c->ccon.resize(n);
+  for (int j = 0; j < n; ++j)
+    cam_consts_host(views[j], c->disp.width, c->disp.height, &c->cams[j], &c->ccon[j]);
+  c->znear = znear;
+  c->has_rig = true;
+  c->has_frame = false;
+  return CR_OK;
+}
+
+cr_status cr_make_orbit_rig(const cr_display* d, const float look_at[3], const float up[3],
+                            float radius, float height, float yaw_deg, float pitch_deg,
+                            float fov_y_deg, cr_camera* out) {
+  if (!d || !look_at || !up || !out || d->num_views < 1 || d->height < 1) return CR_ERR_INVALID_ARG;
+  const int N = d->num_views;
+  const double pi = 3.14159265358979323846;
+  const double fy = d->height / (2.0 * std::tan(fov_y_deg * pi / 360.0));
+  for (int j = 0; j < N; ++j) {
+    const double a = N > 1 ? (-d->view_cone / 2.0 + d->view_cone * j / (N - 1)) : 0.0;
+    const double th = (yaw_deg + a) * pi / 180.0, ph = pitch_deg * pi / 180.0;
+    const double C[3] = {look_at[0] + radius * std::sin(th) * std::cos(ph),
+                         look_at[1] + height + radius * std::sin(ph),
+                         look_at[2] + radius * std::cos(th) * std::cos(ph)};
+    double f[3] = {look_at[0] - C[0], look_at[1] - C[1], look_at[2] - C[2]};
+    double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    for (double& v : f) v /= fn;
+    double x[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2],
+                   f[0] * up[1] - f[1] * up[0]};
+    double xn = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+    for (double& v : x) v /= xn;
+    const double y[3] = {f[1] * x[2] - f[2] * x[1], f[2] * x[0] - f[0] * x[2],
+                         f[0] * x[1] - f[1] * x[0]};
+    const double* rows[3] = {x, y, f};
+    cr_camera& cam = out[j];
+    for (int r = 0; r < 3; ++r) {
+      for (int q = 0; q < 3; ++q) cam.R[r * 3 + q] = (float)rows[r][q];
+      cam.t[r] = (float)(-(rows[r][0] * C[0] + rows[r][1] * C[1] + rows[r][2] * C[2]));
+    }
+    cam.fx = cam.fy = (float)fy;
+    cam.cx = (float)(d->width / 2.0);
+    cam.cy = (float)(d->height / 2.0);
+  }
+  return CR_OK;
+}
+
+cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, size_t out_bytes,
+                               int out_on_device, cr_stats* st) {
+  if (!c || !o || !out) return CR_ERR_INVALID_ARG;
+  if (!c->has_scene || !c->has_display || !c->has_rig)
+    return fail(c, CR_ERR_NOT_READY, "upload Gaussians, set display and rig first");
+  const int N = c->disp.num_views, W = c->disp.width, H = c->disp.height;
+  const int TX = c->TX, TY = c->TY;
+  const int s = o->cluster_size;
+  if (s < 1 || s > kMaxCluster) return fail(c, CR_ERR_INVALID_CONFIG, "cluster_size %d not in 1..32", s);
+  if (o->remap != 0 && o->remap != 1) return fail(c, CR_ERR_INVALID_ARG, "remap must be 0/1");
+  if (o->kernel != 0 && o->kernel != 1) return fail(c, CR_ERR_INVALID_ARG, "kernel must be 0/1");
+  if (o->kernel == 0 && o->remap == 0)
+    return fail(c, CR_ERR_INVALID_ARG, "the staged composite needs remap=1 (use kernel=1)");
+  if (o->output_format != 0 && o->output_format != 1) return fail(c, CR_ERR_INVALID_ARG, "format");
+  for (int u = 0; u < 3; ++u)
+    if (!std::isfinite(o->background[u])) return fail(c, CR_ERR_NONFINITE, "background");
+  int row0 = o->tile_row_begin, row1 = o->tile_row_end;
+  if (row0 == 0 && row1 == 0) row1 = TY;
+  if (row0 < 0 || row1 > TY || row0 >= row1)
+    return fail(c, CR_ERR_INVALID_ARG, "tile rows [%d,%d) outside [0,%d)", row0, row1, TY);
+  const int y0 = row0 * 16, y1 = std::min(H, row1 * 16);
+  const size_t obytes = (size_t)(y1 - y0) * W * 3 * (o->output_format ? 4 : 1);
+  if (out_bytes < obytes) return fail(c, CR_ERR_INVALID_ARG, "out_bytes %zu < %zu", out_bytes, obytes);
+  // O3 clusters
+  const int K = (N + s - 1) / s;
+  int bitK = 0;
+  while ((1 << bitK) < K) ++bitK;
+  bitK = std::max(bitK, 1);
+  if ((long long)TX * TY >= (1LL << (32 - bitK)))
+    return fail(c, CR_ERR_TILE_ID_OVERFLOW, "%d tiles need more than %d bits", TX * TY, 32 - bitK);
+  const long long M = c->M;
+  const long long R = (long long)K * M;
+  if (R > 0xFFFFFFFFLL) return fail(c, CR_ERR_CAPACITY, "K*M = %lld exceeds 2^32", R);
+  cudaSetDevice(c->device);
+  c->launches = 0;
+  c->has_frame = false;
+  cudaStream_t str = c->stream;
+
+  // ---- constants: rig, representatives, frame parameters
+  FrameParams fp{};
+  fp.W = W; fp.H = H; fp.TX = TX; fp.TY = TY; fp.N = N; fp.s = s; fp.K = K; fp.bitK = bitK;
+  fp.row0 = row0; fp.row1 = row1; fp.deg = c->deg; fp.remap = o->remap; fp.M = M;
+  fp.znear = c->znear;
+  for (int u = 0; u < 3; ++u) fp.bg[u] = o->background[u];
+  std::vector<int> rep(K);
+  for (int k = 0; k < K; ++k) rep[k] = std::min(k * s + s / 2, N - 1);
+  CR_CUDA(c, cudaMemcpyToSymbolAsync(c_cams, c->cams.data(), sizeof(CamDev) * N, 0,
+                                     cudaMemcpyHostToDevice, str));
+  CR_CUDA(c, cudaMemcpyToSymbolAsync(c_ccon, c->ccon.data(), sizeof(CamConstDev) * N, 0,
+                                     cudaMemcpyHostToDevice, str));
+  CR_CUDA(c, cudaMemcpyToSymbolAsync(c_rep, rep.data(), sizeof(int) * K, 0,
+                                     cudaMemcpyHostToDevice, str));
+  CR_CUDA(c, cudaMemcpyToSymbolAsync(c_fp, &fp, sizeof(fp), 0, cudaMemcpyHostToDevice, str));
+
+  // ---- composite work items (static per display and s)
+  if (o->kernel == 0 && c->chunks_s != s) {
+    const int stride = K + 24;
+    CR_TRY(ensure(c, c->chunks, (size_t)TX * TY * stride * 4));
+    CR_TRY(ensure(c, c->nchunks, (size_t)TX * TY * 4));
+    k_chunks_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
+        P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),
+        P_<uint32_t>(c->nchunks), stride, W, TX, TY, s);
+    CR_LAUNCHED(c);
+    c->chunks_s = s;
+    c->chunk_stride = stride;
+  }
+
+  uint32_t* sc = P_<uint32_t>(c->scalars);  // [0] nvis [1] P [2] tmp [3] overflow [4] flag
+  // counters: [0] near [1] degenerate [2] opacity [3] evals (u64 at byte 32)
+  unsigned long long* counters = (unsigned long long*)(sc + 8);
+  CR_CUDA(c, cudaMemsetAsync(sc, 0, 64, str));
+  CR_TRACE(c, "constants+chunks");
+  CR_CUDA(c, cudaEventRecord(c->ev[0], str));
+
+  // ---- a4 preprocess + count
+  const size_t Rz = (size_t)std::max<long long>(R, 1);
+  CR_TRY(ensure(c, c->rec0, Rz * 16));
+  CR_TRY(ensure(c, c->rec1, Rz * 16));
+  CR_TRY(ensure(c, c->cnt, Rz * 4));
+  CR_TRY(ensure(c, c->dkey, Rz * 4));
+  CR_TRY(ensure(c, c->ka, Rz * 4));
+  CR_TRY(ensure(c, c->va, Rz * 4));
+  CR_TRY(ensure(c, c->kb, Rz * 4));
+  CR_TRY(ensure(c, c->vb, Rz * 4));
+  CR_TRY(ensure(c, c->offs, Rz * 4));
+  uint32_t nvis = 0;
+  if (M > 0) {
+    const unsigned g = grid_for(M, 128);
+    switch (c->deg) {
+      case 0: k_preprocess<0><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
+      case 1: k_preprocess<1><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
+      case 2: k_preprocess<2><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
+      default: k_preprocess<3><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
+    }
+    CR_LAUNCHED(c);
+    CR_TRACE(c, "preprocess");
+    // compaction of visible records, (k, i) order
+    CR_TRY(dev_scan(c, Scan::InFlag{P_<uint32_t>(c->cnt)},
+                    Scan::OutCompact{P_<uint32_t>(c->dkey), P_<uint32_t>(c->ka), P_<uint32_t>(c->va)},
+                    R, sc + 0));
+    CR_TRY(read_u32(c, sc + 0, &nvis));
+    CR_TRACE(c, "compaction");
+  }
+  CR_CUDA(c, cudaEventRecord(c->ev[1], str));
+
+  // ---- a7 depth presort: stable by depth bits (4 passes), then by k (1 pass)
+  uint32_t *kA = P_<uint32_t>(c->ka), *vA = P_<uint32_t>(c->va);
+  uint32_t *kB = P_<uint32_t>(c->kb), *vB = P_<uint32_t>(c->vb);
+  for (int pass = 0; pass < 4; ++pass) {
+    CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, 8 * pass, false, 1, true));
+    std::swap(kA, kB);
+    std::swap(vA, vB);
+  }
+  if (K > 1) {
+    CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, 0, true, (unsigned long long)M, false));
+    std::swap(vA, vB);
+  }
+  const uint32_t* rec_sorted = vA;  // (k, depth, i)-ordered record indices r
+  CR_TRACE(c, "depth presort");
+  CR_CUDA(c, cudaEventRecord(c->ev[2], str));
+
+  // ---- a6 offsets + emit
+  uint32_t P = 0;
+  if (nvis > 0) {
+    CR_TRY(dev_scan(c, Scan::InGather{P_<uint32_t>(c->cnt), rec_sorted},
+                    Scan::OutStore{P_<uint32_t>(c->offs)}, nvis, sc + 1));
+    CR_TRY(read_u32(c, sc + 1, &P));
+    uint32_t ovf = 0;
+    CR_TRY(read_u32(c, sc + 3, &ovf));
+    if (ovf) return fail(c, CR_ERR_CAPACITY, "pair count exceeds 2^32-1");
+  }
+  const size_t Pz = std::max<size_t>(P, 1);
+  CR_TRY(ensure(c, c->pta, Pz * 4));
+  CR_TRY(ensure(c, c->pva, Pz * 4));
+  CR_TRY(ensure(c, c->ptb, Pz * 4));
+  CR_TRY(ensure(c, c->pvb, Pz * 4));
+  uint32_t *tA = P_<uint32_t>(c->pta), *pA = P_<uint32_t>(c->pva);
+  uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
+  if (P > 0) {
+    k_emit<<<grid_for(nvis, 128), 128, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis,
+                                                  P_<float4>(c->mean4), P_<float4>(c->cov8), tA, pA);
+    CR_LAUNCHED(c);
+  }
+  CR_TRACE(c, "offsets+emit");
+  CR_CUDA(c, cudaEventRecord(c->ev[3], str));
+
+  // ---- a7 stable tile sort + a8 ranges
+  int tbits = 1;
+  while ((1LL << tbits) < (long long)TX * TY) ++tbits;
+  for (int sh = 0; sh < tbits; sh += 8) {
+    CR_TRY(radix_pass(c, tA, pA, tB, pB, P, sh, false, 1, true));
+    std::swap(tA, tB);
+    std::swap(pA, pB);
+  }
+  const size_t nSE = (size_t)TX * TY * K;
+  CR_TRY(ensure(c, c->S, nSE * 4));
+  CR_TRY(ensure(c, c->E, nSE * 4));
+  CR_CUDA(c, cudaMemsetAsync(c->S.p, 0, nSE * 4, str));
+  CR_CUDA(c, cudaMemsetAsync(c->E.p, 0, nSE * 4, str));
+  if (P > 0) {
+    k_ranges<<<grid_for(P, 256), 256, 0, str>>>(tA, pA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
+    CR_LAUNCHED(c);
+  }
+  CR_TRACE(c, "tile sort+ranges");
+  CR_CUDA(c, cudaEventRecord(c->ev[4], str));
+
+  // ---- a9 composite
+  void* dst = out;
+  if (!out_on_device) {
+    CR_TRY(ensure(c, c->stage_out, obytes));
+    dst = c->stage_out.p;
+  }
+  const unsigned ntile = (unsigned)((row1 - row0) * TX);
+  const float4* m4 = P_<float4>(c->mean4);
+  const bool count = (o->flags & CR_FLAG_COUNT_EVALS) != 0;
+  unsigned long long* evals = counters + 3;
+#define CR_STAGED(F, CNT)                                                                     \
+  k_composite_staged<F, CNT><<<ntile, kCompWarps * 32, 0, str>>>(                             \
+      P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
+      P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
+      P_<float4>(c->rec0), P_<float4>(c->rec1), m4, dst, evals)
+#define CR_THREAD(F, CNT)                                                                     \
+  k_composite_thread<F, CNT><<<ntile, kTileSub, 0, str>>>(                                    \
+      P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,    \
+      P_<float4>(c->rec0), P_<float4>(c->rec1), m4, dst, evals)
+  const int fmt = o->output_format;
+  if (o->kernel == 0) {
+    if (fmt == 0) { if (count) CR_STAGED(0, true); else CR_STAGED(0, false); }
+    else          { if (count) CR_STAGED(1, true); else CR_STAGED(1, false); }
+  } else {
+    if (fmt == 0) { if (count) CR_THREAD(0, true); else CR_THREAD(0, false); }
+    else          { if (count) CR_THREAD(1, true); else CR_THREAD(1, false); }
+  }
+#undef CR_STAGED
+#undef CR_THREAD
+  CR_LAUNCHED(c);
+  CR_TRACE(c, "composite");
+  CR_CUDA(c, cudaEventRecord(c->ev[5], str));
+  if (!out_on_device) {
+    CR_CUDA(c, cudaMemcpyAsync(out, dst, obytes, cudaMemcpyDeviceToHost, str));
+    CR_CUDA(c, cudaStreamSynchronize(str));
+  }
+  c->K = K;
+  c->bitK = bitK;
+  c->P = P;
+  c->nvis = nvis;
+  c->final_t = tA;
+  c->final_v = pA;
+  c->has_frame = true;
+  if (st) {
+    CR_CUDA(c, cudaStreamSynchronize(str));
+    std::memset(st, 0, sizeof(*st));
+    unsigned long long cnts[4] = {0, 0, 0, 0};
+    CR_CUDA(c, cudaMemcpy(cnts, counters, sizeof(cnts), cudaMemcpyDeviceToHost));
+    st->pairs = P;
+    st->visible_ik = nvis;
+    st->culled_near = (int64_t)cnts[0];
+    st->culled_degenerate = (int64_t)cnts[1];
+    st->culled_opacity = (int64_t)cnts[2];
+    st->evals = (int64_t)cnts[3];
+    st->num_clusters = K;
+    st->bit_k = bitK;
+    st->launches = c->launches;
+    float ms[5];
+    for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&ms[q], c->ev[q], c->ev[q + 1]);
+    st->ms_preprocess = ms[0];
+    st->ms_sort = ms[1] + ms[3];
+    st->ms_bin = ms[2];
+    st->ms_composite = ms[4];
+    cudaEventElapsedTime(&st->ms_total, c->ev[0], c->ev[5]);
+    st->device_bytes = c->device_bytes;
+  }
+  return CR_OK;
+}
+
+// ---------------------------------------------------------------- introspection
+static cr_status copy_out(cr_ctx* c, void* dst, const void* src, size_t count, size_t elt,
+                          size_t* n) {
+  if (!n) return CR_ERR_INVALID_ARG;
+  if (!dst) { *n = count; return CR_OK; }
+  if (*n < count) return fail(c, CR_ERR_INVALID_ARG, "capacity %zu < %zu", *n, count);
+  if (count) {
+    CR_CUDA(c, cudaStreamSynchronize(c->stream));
+    CR_CUDA(c, cudaMemcpy(dst, src, count * elt, cudaMemcpyDeviceToHost));
+  }
+  *n = count;
+  return CR_OK;
+}
+
+cr_status cr_get_view_map(cr_ctx* c, uint8_t* dst, size_t* n) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  if (!c->has_display) return fail(c, CR_ERR_NOT_READY, "no display");
+  cudaSetDevice(c->device);
+  return copy_out(c, dst, c->V.p, (size_t)c->disp.width * c->disp.height * 3, 1, n);
+}
+
+cr_status cr_get_remap(cr_ctx* c, uint16_t* dst, size_t* n) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  if (!c->has_display) return fail(c, CR_ERR_NOT_READY, "no display");
+  cudaSetDevice(c->device);
+  return copy_out(c, dst, c->psi.p, (size_t)c->TX * c->TY * kTileSub, 2, n);
+}
+
+cr_status cr_get_sorted_pairs(cr_ctx* c, uint64_t* keys, uint32_t* pay, size_t* n) {
+  if (!c || !n) return CR_ERR_INVALID_ARG;
+  if (!c->has_frame) return fail(c, CR_ERR_NOT_READY, "no frame rendered");
+  if (!keys || !pay) { *n = c->P; return CR_OK; }
+  if (*n < c->P) return fail(c, CR_ERR_INVALID_ARG, "capacity");
+  cudaSetDevice(c->device);
+  if (c->P) {
+    DevBuf kb, pb;
+    CR_TRY(ensure(c, kb, (size_t)c->P * 8));
+    cr_status s = ensure(c, pb, (size_t)c->P * 4);
+    if (s != CR_OK) { release(kb); return s; }
+    k_make_keys<<<grid_for(c->P, 256), 256, 0, c->stream>>>(
+        c->final_t, c->final_v, P_<uint32_t>(c->dkey), c->P, P_<unsigned long long>(kb),
+        P_<uint32_t>(pb));
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(keys, kb.p, (size_t)c->P * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(pay, pb.p, (size_t)c->P * 4, cudaMemcpyDeviceToHost);
+    c->device_bytes -= (long long)(kb.bytes + pb.bytes);
+    release(kb);
+    release(pb);
+    if (e != cudaSuccess) return fail(c, CR_ERR_CUDA, "get_sorted_pairs: %s", cudaGetErrorString(e));
+  }
+  *n = c->P;
+  return CR_OK;
+}
+
+cr_status cr_get_ranges(cr_ctx* c, uint32_t* S, uint32_t* E, size_t* n) {
+  if (!c || !n) return CR_ERR_INVALID_ARG;
+  if (!c->has_frame) return fail(c, CR_ERR_NOT_READY, "no frame rendered");
+  const size_t cnt = (size_t)c->TX * c->TY * c->K;
+  if (!S || !E) { *n = cnt; return CR_OK; }
+  size_t cap = *n;
+  CR_TRY(copy_out(c, S, c->S.p, cnt, 4, n));
+  *n = cap;
+  return copy_out(c, E, c->E.p, cnt, 4, n);
+}
+
+cr_status cr_get_depths(cr_ctx* c, float* dst, size_t* n) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  if (!c->has_frame) return fail(c, CR_ERR_NOT_READY, "no frame rendered");
+  cudaSetDevice(c->device);
+  return copy_out(c, dst, c->dkey.p, (size_t)c->K * c->M, 4, n);
+}
+
+cr_status cr_get_counts(cr_ctx* c, uint32_t* dst, size_t* n) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  if (!c->has_frame) return fail(c, CR_ERR_NOT_READY, "no frame rendered");
+  cudaSetDevice(c->device);
+  return copy_out(c, dst, c->cnt.p, (size_t)c->K * c->M, 4, n);
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// cr_composite.cuh — a9 subpixel compositing (Eqs.9-10; Alg.2
+// Alpha-Blend).
+//
+// k_composite_staged (B200 design, default):
+//   CTA per 16x16 tile, 8 warps pulling "cluster-aligned warp chunks" (<= 32
+//   consecutive Psi ranks of one cluster k) from a shared-memory queue.  Per
+//   chunk the warp streams list (t,k) in 32-entry batches: lane l gathers
+//   entry l's record and world mean once, projects the mean for each of the
+//   <= 8 distinct views present in the chunk (per-view mu2D_{i,j}, Eq.5), and
+//   stages everything in shared memory; then every lane walks the batch from
+//   shared memory (broadcast reads) for its own subpixel.  A warp ballot ends
+//   the list as soon as every lane has saturated.  Results go to a smem tile
+//   and leave in coalesced row stores.
+// k_composite_thread (the paper's design): one thread per subpixel rank r,
+//   x = Psi(r) (remap=1) or raster order (remap=0), private list traversal
+//   with direct gathers and a direct scattered store.
+#pragma once
+#include "cr_device.cuh"
+
+namespace cr {
+
+constexpr int kCompWarps = 8;
+constexpr int kSlots = 8;  // distinct views staged per pass of a chunk
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Tolerance-path per-view mean (fast FMA / reciprocal); far away when the
+// view cannot see the Gaussian (Z12) so that alpha underflows to 0.
+__device__ __forceinline__ float2 mean2d_fast(const CamDev& c, float mx, float my, float mz) {
+  const float px = fmaf(c.R[0], mx, fmaf(c.R[1], my, fmaf(c.R[2], mz, c.t[0])));
+  const float py = fmaf(c.R[3], mx, fmaf(c.R[4], my, fmaf(c.R[5], mz, c.t[1])));
+  const float pz = fmaf(c.R[6], mx, fmaf(c.R[7], my, fmaf(c.R[8], mz, c.t[2])));
+  if (!(pz >= c_fp.znear)) return make_float2(1e18f, 1e18f);
+  const float iz = __frcp_rn(pz);
+  return make_float2(fmaf(c.fx, px * iz, c.cx), fmaf(c.fy, py * iz, c.cy));
+}
+
+// One blend step (Eq.10 alpha, Eq.9 accumulation; 0.99 clamp, 1/255 skip,
+// stop before blending when T(1-alpha) < 1e-4 — Z9).
+__device__ __forceinline__ void blend_step(const float4 g, const float2 m, const float col,
+                                           const float px, const float py, float& T, float& C,
+                                           bool& done) {
+  const float dx = m.x - px, dy = m.y - py;
+  const float q = fmaf(g.x * dx, dx, fmaf(g.z * dy, dy, g.y * dx * dy));  // power*log2(e)
+  if (q <= 0.0f) {
+    const float alpha = fminf(0.99f, ex2_approx(q + g.w));
+    if (alpha >= (1.0f / 255.0f)) {
+      const float Tn = T * (1.0f - alpha);
+      if (Tn < 1e-4f) {
+        done = true;
+      } else {
+        C = fmaf(col, alpha * T, C);
+        T = Tn;
+      }
+    }
+  }
+}
+
+template <int FMT>
+__device__ __forceinline__ void store_tile(const float* s_out, void* out, int tx, int ty, int W,
+                                           int H, int y_band0) {
+  const int nx = min(16, W - tx * 16), ny = min(16, H - ty * 16);
+  if (FMT == 0) {
+    uint8_t* o = (uint8_t*)out;
+    const int rowb = nx * 3;
+    for (int q = threadIdx.x; q < ny * rowb; q += blockDim.x) {
+      const int ly = q / rowb, b = q % rowb;
+      const float v = s_out[ly * 48 + b];
+      const float cl = fminf(fmaxf(v, 0.0f), 1.0f);
+      const uint8_t u8 = (uint8_t)floorf(__fadd_rn(__fmul_rn(cl, 255.0f), 0.5f));
+      o[((long long)(ty * 16 + ly - y_band0) * W + tx * 16) * 3 + b] = u8;
+    }
+  } else {
+    float* o = (float*)out;
+    const int rowb = nx * 3;
+    for (int q = threadIdx.x; q < ny * rowb; q += blockDim.x) {
+      const int ly = q / rowb, b = q % rowb;
+      o[((long long)(ty * 16 + ly - y_band0) * W + tx * 16) * 3 + b] = s_out[ly * 48 + b];
+    }
+  }
+}
+
+// Instrumentation (CR_FLAG_COUNT_EVALS): add this thread's evaluation count.
+__device__ __forceinline__ void add_evals(unsigned long long* evals, unsigned long long n) {
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(evals, n);
+}
+
+template <int FMT, bool COUNT>
+__global__ void __launch_bounds__(kCompWarps * 32) k_composite_staged(
+    const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,
+    const uint32_t* __restrict__ chunks, const uint32_t* __restrict__ nchunks, int stride,
+    const uint32_t* __restrict__ S, const uint32_t* __restrict__ E,
+    const uint32_t* __restrict__ vals, const float4* __restrict__ rec0,
+    const float4* __restrict__ rec1, const float4* __restrict__ mean4, void* __restrict__ out,
+    unsigned long long* __restrict__ evals) {
+  __shared__ float4 s_rec[kCompWarps][32];
+  __shared__ float4 s_col[kCompWarps][32];
+  __shared__ float2 s_mu[kCompWarps][kSlots][32];
+  __shared__ float s_out[kTileSub];
+  __shared__ int s_next;
+  const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
+  const long long M = c_fp.M;
+  const int t = c_fp.row0 * TX + blockIdx.x;
+  const int tx = t % TX, ty = t / TX;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_next = 0;
+  __syncthreads();
+  const int nch = nchunks[t];
+  const uint32_t* ch_t = chunks + (long long)t * stride;
+  const uint16_t* ps = psi + (long long)t * kTileSub;
+  unsigned long long nev = 0;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&s_next, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nch) break;
+    const uint32_t ch = ch_t[c];
+    const int start = ch & 1023, len = ((ch >> 10) & 63) + 1, k = ch >> 16;
+    // this lane's subpixel
+    int l = 0, u = 0, j = 0;
+    float px = 0.f, py = 0.f;
+    const bool mine = lane < len;
+    if (mine) {
+      l = ps[start + lane];
+      const int ly = l / 48, rem = l % 48, lx = rem / 3;
+      u = rem % 3;
+      const int x = tx * 16 + lx, y = ty * 16 + ly;
+      j = V[((long long)y * W + x) * 3 + u];
+      px = (float)x + 0.5f;
+      py = (float)y + 0.5f;
+    }
+    const int jlo = __shfl_sync(0xffffffffu, j, 0);
+    const int jhi = __shfl_sync(0xffffffffu, j, len - 1);
+    const int nsl = jhi - jlo + 1;
+    const int slot = j - jlo;
+    const uint32_t e0 = S[t * K + k], e1 = E[t * K + k];
+    const long long kM = (long long)k * M;
+    for (int g0 = 0; g0 < nsl; g0 += kSlots) {
+      const bool active = mine && slot >= g0 && slot < g0 + kSlots;
+      if (!__any_sync(0xffffffffu, active)) continue;
+      const int ns = min(kSlots, nsl - g0);
+      float T = 1.0f, C = 0.0f;
+      bool done = !active;
+      for (uint32_t b = e0; b < e1; b += 32) {
+        const uint32_t e = b + lane;
+        if (e < e1) {
+          const uint32_t r = vals[e];
+          const float4 m = mean4[(long long)r - kM];
+          s_rec[w][lane] = rec0[r];
+          s_col[w][lane] = rec1[r];
+          for (int v = 0; v < ns; ++v) s_mu[w][v][lane] = mean2d_fast(c_cams[jlo + g0 + v], m.x, m.y, m.z);
+        }
+        __syncwarp();
+        const int n = min(32u, e1 - b);
+        if (!done) {
+          const int sl = slot - g0;
+          for (int q = 0; q < n; ++q) {
+            const float4 g = s_rec[w][q];
+            const float2 mu = s_mu[w][sl][q];
+            const float col = (&s_col[w][q].x)[u];
+            blend_step(g, mu, col, px, py, T, C, done);
+            if (COUNT) ++nev;
+            if (done) break;
+          }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        __syncwarp();
+      }
+      __syncwarp();
+      if (active) s_out[l] = C + c_fp.bg[u] * T;
+    }
+  }
+  if (COUNT) add_evals(evals, nev);
+  __syncthreads();
+  store_tile<FMT>(s_out, out, tx, ty, W, H, c_fp.row0 * 16);
+}
+
+template <int FMT, bool COUNT>
+__global__ void __launch_bounds__(kTileSub) k_composite_thread(
+    const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,
+    const uint32_t* __restrict__ S, const uint32_t* __restrict__ E,
+    const uint32_t* __restrict__ vals, const float4* __restrict__ rec0,
+    const float4* __restrict__ rec1, const float4* __restrict__ mean4, void* __restrict__ out,
+    unsigned long long* __restrict__ evals) {
+  const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K, s = c_fp.s;
+  const long long M = c_fp.M;
+  const int t = c_fp.row0 * TX + blockIdx.x;
+  const int tx = t % TX, ty = t / TX;
+  const int r = threadIdx.x;
+  int l = r;
+  if (c_fp.remap) l = psi[(long long)t * kTileSub + r];  // x^ = Psi(r)
+  const int ly = l / 48, rem = l % 48, lx = rem / 3, u = rem % 3;
+  const int x = tx * 16 + lx, y = ty * 16 + ly;
+  const bool in_panel = l != 0xFFFF && x < W && y < H;
+  if (!in_panel) return;
+  const int j = V[((long long)y * W + x) * 3 + u];  // j = V[x^]
+  const int k = j / s;                                // k = GetClusterID(j)
+  const uint32_t e0 = S[t * K + k], e1 = E[t * K + k];
+  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const CamDev& cam = c_cams[j];
+  const long long kM = (long long)k * M;
+  float T = 1.0f, C = 0.0f;
+  bool done = false;
+  unsigned long long nev = 0;
+  for (uint32_t e = e0; e < e1 && !done; ++e) {
+    if (COUNT) ++nev;
+    const uint32_t rr = vals[e];
+    const float4 m = mean4[(long long)rr - kM];
+    const float2 mu = mean2d_fast(cam, m.x, m.y, m.z);
+    const float4 g = rec0[rr];
+    const float4 cl = rec1[rr];
+    blend_step(g, mu, (&cl.x)[u], px, py, T, C, done);
+  }
+  if (COUNT) atomicAdd(evals, nev);
+  const float v = C + c_fp.bg[u] * T;
+  const long long o = ((long long)(y - c_fp.row0 * 16) * W + x) * 3 + u;
+  if (FMT == 0) {
+    const float cl = fminf(fmaxf(v, 0.0f), 1.0f);
+    ((uint8_t*)out)[o] = (uint8_t)floorf(__fadd_rn(__fmul_rn(cl, 255.0f), 0.5f));
+  } else {
+    ((float*)out)[o] = v;
+  }
+}
+
+}  // namespace cr

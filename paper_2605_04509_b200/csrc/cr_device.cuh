@@ -1,0 +1,156 @@
+// cr_device.cuh — device-side state and exact-arithmetic helpers of the
+// CoherentRaster B200 path.  Included once by cr_all.cu (unity build, so the
+// __constant__ rig is visible to every kernel without -rdc).
+//
+// Exactness rule (DESIGN.md §3 "exact path"): everything that decides a view
+// index, a sort key or a tile list is computed with explicitly rounded IEEE
+// intrinsics (__fadd_rn/__fmul_rn/__fdiv_rn/__fsqrt_rn; fp64 __d*_rn for the
+// view map and Sigma3D), so ptxas can neither contract to FMA nor
+// approximate, and min/max are plain compares.  Colours, conics and alpha are
+// "tolerance path" values and use fast FMA / MUFU math.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cr {
+
+constexpr int kTile = 16;
+constexpr int kTileSub = kTile * kTile * 3;  // 768 subpixels per tile
+constexpr int kMaxViews = 255;
+constexpr int kMaxCluster = 32;
+
+struct CamDev {
+  float R[9], t[3], fx, fy, cx, cy;  // 64 B
+};
+struct CamConstDev {
+  float limxp, limxn, limyp, limyn;  // EWA frustum clamp (O6)
+  float C[3];                        // camera centre -R^T t (O11)
+  float pad;
+};
+struct FrameParams {
+  int W, H, TX, TY, N, s, K, bitK;
+  int row0, row1;  // tile-row band [row0, row1)
+  int deg;
+  int remap;
+  long long M;
+  float znear;
+  float bg[3];
+};
+
+__constant__ CamDev c_cams[kMaxViews];
+__constant__ CamConstDev c_ccon[kMaxViews];
+__constant__ int c_rep[kMaxViews];
+__constant__ FrameParams c_fp;
+
+// ---------------------------------------------------------------- exact ops
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float xdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float xsqrt(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ float xmin(float a, float b) { return (b < a) ? b : a; }
+__device__ __forceinline__ float xmax(float a, float b) { return (a < b) ? b : a; }
+__device__ __forceinline__ int clamp_to_int(float v, float lo, float hi) {
+  if (!(v >= lo)) v = lo;
+  if (v > hi) v = hi;
+  return (int)v;
+}
+
+struct F3 {
+  float x, y, z;
+};
+
+// O5: camera-space point, each product/sum rounded in the written order.
+__device__ __forceinline__ F3 cam_point_exact(const CamDev& c, float mx, float my, float mz) {
+  F3 p;
+  p.x = xadd(xadd(xadd(xmul(c.R[0], mx), xmul(c.R[1], my)), xmul(c.R[2], mz)), c.t[0]);
+  p.y = xadd(xadd(xadd(xmul(c.R[3], mx), xmul(c.R[4], my)), xmul(c.R[5], mz)), c.t[1]);
+  p.z = xadd(xadd(xadd(xmul(c.R[6], mx), xmul(c.R[7], my)), xmul(c.R[8], mz)), c.t[2]);
+  return p;
+}
+// Eq.5: mu2D = (fx * (px/pz) + cx, fy * (py/pz) + cy)
+__device__ __forceinline__ void mean2d_exact(const CamDev& c, const F3& p, float& ox, float& oy) {
+  ox = xadd(xmul(c.fx, xdiv(p.x, p.z)), c.cx);
+  oy = xadd(xmul(c.fy, xdiv(p.y, p.z)), c.cy);
+}
+
+// O6: EWA Sigma2D at camera c (gsplat classic: +0.3, no compensation).
+// S6 = {00, 01, 02, 11, 12, 22}.  Returns det > 0.
+__device__ __forceinline__ bool cov2d_exact(const CamDev& c, const CamConstDev& k, const F3& p,
+                                            const float* S6, float& a, float& b, float& cc,
+                                            float& det) {
+  const float txz = xdiv(p.x, p.z), tyz = xdiv(p.y, p.z);
+  const float tx = xmul(p.z, xmin(k.limxp, xmax(-k.limxn, txz)));
+  const float ty = xmul(p.z, xmin(k.limyp, xmax(-k.limyn, tyz)));
+  const float zz = xmul(p.z, p.z);
+  const float J00 = xdiv(c.fx, p.z), J02 = -xdiv(xmul(c.fx, tx), zz);
+  const float J11 = xdiv(c.fy, p.z), J12 = -xdiv(xmul(c.fy, ty), zz);
+  float T0[3], T1[3];
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    T0[col] = xadd(xmul(J00, c.R[col]), xmul(J02, c.R[6 + col]));
+    T1[col] = xadd(xmul(J11, c.R[3 + col]), xmul(J12, c.R[6 + col]));
+  }
+  const float S[3][3] = {{S6[0], S6[1], S6[2]}, {S6[1], S6[3], S6[4]}, {S6[2], S6[4], S6[5]}};
+  float U0[3], U1[3];
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    U0[col] = xadd(xadd(xmul(T0[0], S[0][col]), xmul(T0[1], S[1][col])), xmul(T0[2], S[2][col]));
+    U1[col] = xadd(xadd(xmul(T1[0], S[0][col]), xmul(T1[1], S[1][col])), xmul(T1[2], S[2][col]));
+  }
+  a = xadd(xadd(xmul(U0[0], T0[0]), xmul(U0[1], T0[1])), xmul(U0[2], T0[2]));
+  b = xadd(xadd(xmul(U0[0], T1[0]), xmul(U0[1], T1[1])), xmul(U0[2], T1[2]));
+  cc = xadd(xadd(xmul(U1[0], T1[0]), xmul(U1[1], T1[1])), xmul(U1[2], T1[2]));
+  a = xadd(a, 0.3f);
+  cc = xadd(cc, 0.3f);
+  det = xsub(xmul(a, cc), xmul(b, b));
+  return det > 0.0f;
+}
+
+// O7 (AccuTile reading): row range of one view's ellipse {d^T Sigma^-1 d <= tau}.
+struct ViewRows {
+  float mx, my, ex, ey;
+  int ty0, ty1;
+};
+__device__ __forceinline__ ViewRows view_rows(float mx, float my, float a, float c, float tau,
+                                              int TY) {
+  ViewRows v;
+  v.mx = mx;
+  v.my = my;
+  v.ex = xsqrt(xmul(tau, a));
+  v.ey = xsqrt(xmul(tau, c));
+  v.ty0 = clamp_to_int(ceilf(xdiv(xsub(xsub(my, v.ey), 15.5f), 16.0f)), 0.0f, (float)TY);
+  v.ty1 = clamp_to_int(floorf(xdiv(xsub(xadd(my, v.ey), 0.5f), 16.0f)), -1.0f, (float)(TY - 1));
+  return v;
+}
+// Tile columns [tx0, tx1] of row ty; false when the row band misses the ellipse.
+__device__ __forceinline__ bool view_row_cols(const ViewRows& v, float a, float b, float c,
+                                              float det, float tau, int ty, int TX, int& tx0,
+                                              int& tx1) {
+  const float dlo = xmax(xsub(xadd(xmul(16.0f, (float)ty), 0.5f), v.my), -v.ey);
+  const float dhi = xmin(xsub(xadd(xmul(16.0f, (float)ty), 15.5f), v.my), v.ey);
+  if (dlo > dhi) return false;
+  const float dyR = xdiv(xmul(b, v.ex), a);
+  const float dyL = -dyR;
+  const float tc = xmul(tau, c);
+  const float hlo = xsqrt(xmax(0.0f, xmul(det, xsub(tc, xmul(dlo, dlo)))));
+  const float hhi = xsqrt(xmax(0.0f, xmul(det, xsub(tc, xmul(dhi, dhi)))));
+  float right, left;
+  if (dlo <= dyR && dyR <= dhi) {
+    right = v.ex;
+  } else {
+    right = xmax(xdiv(xadd(xmul(b, dlo), hlo), c), xdiv(xadd(xmul(b, dhi), hhi), c));
+  }
+  if (dlo <= dyL && dyL <= dhi) {
+    left = -v.ex;
+  } else {
+    left = xmin(xdiv(xsub(xmul(b, dlo), hlo), c), xdiv(xsub(xmul(b, dhi), hhi), c));
+  }
+  right = xadd(v.mx, right);
+  left = xadd(v.mx, left);
+  tx0 = clamp_to_int(ceilf(xdiv(xsub(left, 15.5f), 16.0f)), 0.0f, (float)TX);
+  tx1 = clamp_to_int(floorf(xdiv(xsub(right, 0.5f), 16.0f)), -1.0f, (float)(TX - 1));
+  return true;
+}
+
+}  // namespace cr

@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bit-exact: view map V, Psi, per-(i,k) depths and tile
+counts, sorted 64-bit keys + payloads, ranges.  Images: RGB8 max |diff| <= 2
+levels and float PSNR >= 50 dB (BASELINE.json north_star tolerance)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_04509_b200 import synthetic as sy
+
+pytestmark = pytest.mark.gpu
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return math.inf if mse == 0 else 10 * math.log10(1.0 / mse)
+
+
+def make_pair(scene, W, H, N, Lx, slant, Koff, cams, znear=0.01, nthreads=0):
+    from paper_2605_04509_b200 import CoherentRaster
+    g = CoherentRaster(0)
+    g.upload_gaussians(scene)
+    g.set_display(W, H, N, Lx, slant, Koff)
+    g.set_camera_rig(cams, znear)
+    o = oracle.Oracle(nthreads=nthreads)
+    o.set_scene(scene)
+    o.set_display(W, H, N, Lx, slant=slant, center_offset=Koff)
+    o.set_rig(cams, znear)
+    return g, o
+
+
+def check_frame(g, o, s, rows=None, bg=(0.0, 0.0, 0.0), kernel=None, remap=True, check_pairs=True):
+    r0, r1 = rows if rows else (0, 0)
+    o.render(s=s, row0=r0, row1=r1, bg=bg)
+    img_f = g.render(cluster_size=s, remap=remap, kernel=kernel, background=bg,
+                     output_format="float", rows=rows, stats=True).cpu().numpy()
+    st = g.last_stats
+    K = o.K
+    assert st["num_clusters"] == K and st["bit_k"] == o.bitK
+    assert st["pairs"] == o.num_pairs
+    if check_pairs:
+        kg, pg = g.sorted_pairs()
+        ko, po = o.pairs()
+        assert np.array_equal(kg, ko), "sorted keys differ"
+        assert np.array_equal(pg, po), "payload order differs"
+        Sg, Eg = g.ranges(K)
+        So, Eo = o.ranges()
+        assert np.array_equal(Sg, So) and np.array_equal(Eg, Eo)
+        rec = o.records()
+        vis = rec["state"] == 0
+        assert np.array_equal(g.counts(K)[vis], rec["count"][vis])
+        assert np.array_equal(g.counts(K)[~vis], np.zeros((~vis).sum(), np.uint32))
+        assert np.array_equal(g.depths(K)[vis].view(np.uint32), rec["depth"][vis].view(np.uint32))
+    ref = o.image()
+    assert img_f.shape == ref.shape
+    assert np.all(np.isfinite(img_f))
+    p = psnr(np.clip(img_f, 0, 1), np.clip(ref, 0, 1))
+    assert p >= 50.0, f"PSNR {p:.2f} dB"
+    img8 = g.render(cluster_size=s, remap=remap, kernel=kernel, background=bg,
+                    output_format="rgb8", rows=rows).cpu().numpy()
+    ref8 = oracle.quantize_rgb8(ref)
+    d = np.abs(img8.astype(np.int16) - ref8.astype(np.int16))
+    assert d.max() <= 2, f"max RGB8 diff {d.max()}"
+    return img_f, p
+
+
+@pytest.fixture(scope="module")
+def cfgA_pair():
+    _need_gpu()
+    c = sy.CONFIGS["A"]
+    return make_pair(c.make_scene(), c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset,
+                     c.make_rig())
+
+
+def test_view_map_and_remap_bit_exact(cfgA_pair):
+    g, o = cfgA_pair
+    assert np.array_equal(g.view_map(), o.view_map())
+    assert np.array_equal(g.remap_table(), o.remap(1))
+
+
+@pytest.mark.parametrize("W,H,N,Lx,slant,K", [
+    (3840, 2160, 100, 19.6153, math.atan(0.1852), 7.3),
+    (3840, 2160, 45, 19.6153, math.atan(0.1852), 7.3),
+    (250, 138, 71, 12.37, -0.2, -5.5),
+    (1, 1, 3, 3.0, 0.0, 0.0),
+])
+def test_view_map_remap_displays(W, H, N, Lx, slant, K):
+    _need_gpu()
+    from paper_2605_04509_b200 import CoherentRaster
+    g = CoherentRaster(0)
+    g.set_display(W, H, N, Lx, slant, K)
+    o = oracle.Oracle()
+    o.set_display(W, H, N, Lx, slant=slant, center_offset=K)
+    assert np.array_equal(g.view_map(), o.view_map())
+    assert np.array_equal(g.remap_table(), o.remap(1))
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8])
+def test_config_a_parity(cfgA_pair, s):
+    g, o = cfgA_pair
+    check_frame(g, o, s, bg=(0.05, 0.1, 0.2))
+
+
+def test_config_a_kernels_and_remap_agree(cfgA_pair):
+    # Psi only permutes independent writes: staged (remap) == thread
+    # (remap) == thread (raster order), bit for bit.
+    g, o = cfgA_pair
+    a = g.render(8, remap=True, kernel=0, output_format="float").cpu().numpy()
+    b = g.render(8, remap=True, kernel=1, output_format="float").cpu().numpy()
+    c = g.render(8, remap=False, kernel=1, output_format="float").cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(b, c)
+
+
+def test_band_shards_equal_full_frame(cfgA_pair):
+    g, o = cfgA_pair
+    full = g.render(4, output_format="float").cpu().numpy()
+    kf, pf = g.sorted_pairs()
+    bands = [(0, 3), (3, 4), (4, 9)]
+    parts = []
+    for r0, r1 in bands:
+        parts.append(g.render(4, output_format="float", rows=(r0, r1)).cpu().numpy())
+        kb, pb = g.sorted_pairs()
+        t = (kb >> np.uint64(32 + 1)) // np.uint64(16)
+        sel = ((kf >> np.uint64(33)) // np.uint64(16) >= r0) & ((kf >> np.uint64(33)) // np.uint64(16) < r1)
+        assert np.array_equal(kb, kf[sel]) and np.array_equal(pb, pf[sel])
+        assert np.all((t >= r0) & (t < r1))
+    assert np.array_equal(np.concatenate(parts), full)
+    # and the band frames match the oracle
+    check_frame(g, o, 4, rows=(3, 7))
+
+
+def test_ragged_panel_and_deg3():
+    _need_gpu()
+    W, H, N = 250, 138, 13  # clipped edge tiles in x and y
+    sc = sy.random_scene(3000, 3, seed=9, scale_median=0.04)
+    cams = sy.orbit_rig(N, 10.0, W, H, radius=3.0, height=0.4, fov_y_deg=50.0)
+    g, o = make_pair(sc, W, H, N, 11.3, 0.17, 3.3, cams)
+    for s in (1, 5):
+        check_frame(g, o, s, bg=(0.3, 0.3, 0.3))
+    check_frame(g, o, 5, rows=(2, 9))
+
+
+def test_identical_pose_rig_any_s_equals_s1():
+    _need_gpu()
+    W, H, N = 128, 80, 8
+    sc = sy.random_scene(2000, 1, seed=3, scale_median=0.05)
+    cams = sy.identical_rig(N, W, H, radius=3.0, height=0.3, fov_y_deg=50.0)
+    g, o = make_pair(sc, W, H, N, 9.7, 0.2, 1.0, cams)
+    ref = g.render(1, output_format="float", stats=True).cpu().numpy()
+    P1 = g.last_stats["pairs"]
+    for s in (2, 4, 8):
+        img = g.render(s, output_format="float", stats=True).cpu().numpy()
+        assert np.array_equal(img, ref)
+        assert g.last_stats["pairs"] * N == P1 * (N // s)
+
+
+def test_empty_scene_and_near_plane():
+    _need_gpu()
+    W, H, N = 64, 48, 4
+    cams = sy.orbit_rig(N, 5.0, W, H, radius=2.0, height=0.0)
+    g, o = make_pair(sy.empty_scene(0), W, H, N, 7.0, 0.1, 0.0, cams)
+    img = g.render(2, background=(0.25, 0.5, 1.0), output_format="float").cpu().numpy()
+    assert np.all(img == np.array([0.25, 0.5, 1.0], np.float32))
+    # Gaussians straddling / behind the camera and huge ones: culling paths
+    sc = sy.random_scene(500, 0, seed=4, extent=2.5, scale_median=0.3)
+    g.upload_gaussians(sc)
+    o.set_scene(sc)
+    check_frame(g, o, 2)
+
+
+def test_device_upload_equals_host_upload(cfgA_pair):
+    g, o = cfgA_pair
+    c = sy.CONFIGS["A"]
+    sc = c.make_scene()
+    a = g.render(8, output_format="float").cpu().numpy()
+    g.upload_gaussians({k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v)
+                        for k, v in sc.items()})
+    b = g.render(8, output_format="float").cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_host_output_buffer(cfgA_pair):
+    g, o = cfgA_pair
+    dev = g.render(8).cpu().numpy()
+    host = np.zeros_like(dev)
+    g.render(8, out=host)
+    assert np.array_equal(dev, host)
+
+
+def test_error_codes():
+    _need_gpu()
+    from paper_2605_04509_b200 import CoherentRaster
+    from paper_2605_04509_b200._native import CrError
+    g = CoherentRaster(0)
+    with pytest.raises(CrError, match="NOT_READY"):
+        g.render(8)
+    with pytest.raises(CrError, match="INVALID_CONFIG"):
+        g.set_display(100, 100, 0, 5.0, 0.1, 0.0)
+    with pytest.raises(CrError, match="INVALID_CONFIG"):
+        g.set_display(100, 100, 300, 5.0, 0.1, 0.0)
+    g.set_display(64, 48, 4, 5.0, 0.1, 0.0)
+    with pytest.raises(CrError, match="CONFIG_MISMATCH"):
+        g.set_camera_rig(sy.orbit_rig(3, 5.0, 64, 48))
+    g.set_camera_rig(sy.orbit_rig(4, 5.0, 64, 48))
+    bad = sy.random_scene(10, 0, 0)
+    bad["means"][3, 1] = np.nan
+    with pytest.raises(CrError, match="NONFINITE"):
+        g.upload_gaussians(bad)
+    g.upload_gaussians(sy.random_scene(10, 0, 0))
+    with pytest.raises(CrError, match="INVALID_CONFIG"):
+        g.render(33)
+    with pytest.raises(CrError, match="INVALID_ARG"):
+        g.render(2, rows=(2, 1))
+
+
+def test_config_b_full_size_sampled_tiles():
+    # BASELINE configs[1] at full size (1M Gaussians SH3, 45 views, 4K): bit-exact
+    # pair count and per-(i,k) counts for the whole frame, exact keys and images on
+    # a sample of tiles the oracle composites one by one.
+    _need_gpu()
+    c = sy.CONFIGS["B"]
+    g, o = make_pair(c.make_scene(), c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset,
+                     c.make_rig())
+    rng = np.random.default_rng(0)
+    TX, TY = (c.W + 15) // 16, (c.H + 15) // 16
+    tiles = np.sort(rng.choice(TX * TY, 48, replace=False)).astype(np.int32)
+    o.render(s=8, tiles=tiles)
+    img = g.render(8, output_format="float", stats=True).cpu().numpy()
+    st = g.last_stats
+    assert st["pairs"] == int(o.records()["count"].sum())
+    kg, pg = g.sorted_pairs()
+    tg = (kg >> np.uint64(32 + o.bitK)).astype(np.int64)
+    sel = np.isin(tg, tiles)
+    ko, po = o.pairs()
+    assert np.array_equal(kg[sel], ko) and np.array_equal(pg[sel], po)
+    ref = o.image()
+    for t in tiles:
+        tx, ty = t % TX, t // TX
+        a = img[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16]
+        b = ref[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16]
+        assert np.abs(a - b).max() <= 2.0 / 255
+    a = np.concatenate([img[(t // TX) * 16:(t // TX + 1) * 16, (t % TX) * 16:(t % TX + 1) * 16]
+                        for t in tiles])
+    b = np.concatenate([ref[(t // TX) * 16:(t // TX + 1) * 16, (t % TX) * 16:(t % TX + 1) * 16]
+                        for t in tiles])
+    assert psnr(np.clip(a, 0, 1), np.clip(b, 0, 1)) >= 50.0
