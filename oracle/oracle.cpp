@@ -211,9 +211,10 @@ bool row_cols(float mx, float my, float a, float b, float c, float det, float ta
     float dyR = (b * ex) / a;
     float dyL = -dyR;
     float tc = tau * c;
+    float ic = 1.0f / c;  // reading O7: one rounded reciprocal, then products
     auto h = [&](float dy) { return std::sqrt(mxf(0.0f, det * (tc - dy * dy))); };
-    auto xr = [&](float dy) { return ((b * dy) + h(dy)) / c; };
-    auto xl = [&](float dy) { return ((b * dy) - h(dy)) / c; };
+    auto xr = [&](float dy) { return ((b * dy) + h(dy)) * ic; };
+    auto xl = [&](float dy) { return ((b * dy) - h(dy)) * ic; };
     float right = mx + ((dlo <= dyR && dyR <= dhi) ? ex : mxf(xr(dlo), xr(dhi)));
     float left = mx + ((dlo <= dyL && dyL <= dhi) ? -ex : mnf(xl(dlo), xl(dhi)));
     *tx0 = clamp_to_int(std::ceil((left - 15.5f) / 16.0f), 0.0f, (float)TX);

@@ -57,6 +57,26 @@ struct Scan {  // functors for the generic device scan
       if (v) { ko[ex] = dkey[i]; vo[ex] = (uint32_t)i; }
     }
   };
+  struct OutIdx {  // compaction: write the index of every flagged element
+    uint32_t* o;
+    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
+      if (v) o[ex] = (uint32_t)i;
+    }
+  };
+  struct InCntPos {  // flag: record list[e] has >= 1 tile
+    const uint32_t* cnt;
+    const uint32_t* list;
+    __device__ uint32_t operator()(long long e) const { return cnt[list[e]] > 0u ? 1u : 0u; }
+  };
+  struct OutCompactList {
+    const uint32_t* list;
+    const uint32_t* dkey;
+    uint32_t* ko;
+    uint32_t* vo;
+    __device__ void operator()(long long e, uint32_t ex, uint32_t v) const {
+      if (v) { const uint32_t r = list[e]; ko[ex] = dkey[r]; vo[ex] = r; }
+    }
+  };
   struct InGather {
     const uint32_t* cnt;
     const uint32_t* idx;
@@ -96,7 +116,7 @@ struct cr_ctx {
   std::vector<CamConstDev> ccon;
   float znear = 0.01f;
   // frame buffers
-  DevBuf rec0, rec1, cnt, dkey, offs;
+  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, vlist, slots, elist;
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
   DevBuf bsum, hist, scalars, S, E, stage_out;
@@ -339,7 +359,7 @@ void cr_destroy(cr_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
-                   &c->rec0, &c->rec1, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
+                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->tmp};
   for (DevBuf* b : all) release(*b);
@@ -401,7 +421,7 @@ cr_status cr_upload_gaussians(cr_ctx* c, int64_t M, int deg, const float* means,
   CR_TRY(ensure(c, c->mean4, 16 * (size_t)M));
   CR_TRY(ensure(c, c->cov8, 32 * (size_t)M));
   CR_TRY(ensure(c, c->shsoa, 4 * (size_t)M * nc3));
-  int* flag = P_<int>(c->scalars) + 4;
+  int* flag = P_<int>(c->scalars) + 6;
   CR_CUDA(c, cudaMemsetAsync(flag, 0, 4, c->stream));
   k_upload<<<grid_for(M, 256), 256, 0, c->stream>>>(M, nc3, d_means, d_quats, d_scales, d_op,
                                                      d_tau, d_sh, P_<float4>(c->mean4),
@@ -574,17 +594,20 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     c->chunk_stride = stride;
   }
 
-  uint32_t* sc = P_<uint32_t>(c->scalars);  // [0] nvis [1] P [2] tmp [3] overflow [4] flag
+  uint32_t* sc = P_<uint32_t>(c->scalars);  // [0] nvis [1] P [2] tmp [3] overflow [4] nvis0
   // counters: [0] near [1] degenerate [2] opacity [3] evals (u64 at byte 32)
   unsigned long long* counters = (unsigned long long*)(sc + 8);
   CR_CUDA(c, cudaMemsetAsync(sc, 0, 64, str));
   CR_TRACE(c, "constants+chunks");
   CR_CUDA(c, cudaEventRecord(c->ev[0], str));
 
-  // ---- a4 preprocess + count
+  // ---- a4 preprocess + SH, a6 count, compaction of records with >= 1 tile
   const size_t Rz = (size_t)std::max<long long>(R, 1);
   CR_TRY(ensure(c, c->rec0, Rz * 16));
   CR_TRY(ensure(c, c->rec1, Rz * 16));
+  CR_TRY(ensure(c, c->geom, Rz * 16));
+  CR_TRY(ensure(c, c->vis, Rz * 4));
+  CR_TRY(ensure(c, c->vlist, Rz * 4));
   CR_TRY(ensure(c, c->cnt, Rz * 4));
   CR_TRY(ensure(c, c->dkey, Rz * 4));
   CR_TRY(ensure(c, c->ka, Rz * 4));
@@ -592,22 +615,46 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->kb, Rz * 4));
   CR_TRY(ensure(c, c->vb, Rz * 4));
   CR_TRY(ensure(c, c->offs, Rz * 4));
-  uint32_t nvis = 0;
+  CR_TRY(ensure(c, c->slots, Rz * 32));
+  CR_TRY(ensure(c, c->elist, Rz * 4));
+  int G = 1;
+  while (G < s) G <<= 1;
+  const unsigned bin_grid = (unsigned)(148 * 8);
+  uint32_t nvis = 0, nvis0 = 0;
   if (M > 0) {
     const unsigned g = grid_for(M, 128);
+#define CR_PRE(D)                                                                               \
+  k_preprocess<D><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
+                                      P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
+                                      P_<float4>(c->rec1), P_<float4>(c->geom),                 \
+                                      P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters)
     switch (c->deg) {
-      case 0: k_preprocess<0><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
-      case 1: k_preprocess<1><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
-      case 2: k_preprocess<2><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
-      default: k_preprocess<3><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8), P_<float>(c->shsoa), P_<float4>(c->rec0), P_<float4>(c->rec1), P_<uint32_t>(c->cnt), P_<uint32_t>(c->dkey), counters); break;
+      case 0: CR_PRE(0); break;
+      case 1: CR_PRE(1); break;
+      case 2: CR_PRE(2); break;
+      default: CR_PRE(3); break;
     }
+#undef CR_PRE
     CR_LAUNCHED(c);
     CR_TRACE(c, "preprocess");
-    // compaction of visible records, (k, i) order
-    CR_TRY(dev_scan(c, Scan::InFlag{P_<uint32_t>(c->cnt)},
-                    Scan::OutCompact{P_<uint32_t>(c->dkey), P_<uint32_t>(c->ka), P_<uint32_t>(c->va)},
-                    R, sc + 0));
-    CR_TRY(read_u32(c, sc + 0, &nvis));
+    // visible (i,k) records, (k, i) order
+    CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->vis)}, Scan::OutIdx{P_<uint32_t>(c->vlist)}, R,
+                    sc + 4));
+    CR_TRY(read_u32(c, sc + 4, &nvis0));
+    CR_CUDA(c, cudaMemsetAsync(c->cnt.p, 0, (size_t)R * 4, str));
+    if (nvis0 > 0) {
+      k_count<<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0, G,
+                                                 P_<float4>(c->mean4), P_<float4>(c->geom),
+                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots));
+      CR_LAUNCHED(c);
+      CR_TRACE(c, "count");
+      // records with >= 1 tile in the band -> (depth key, r)
+      CR_TRY(dev_scan(c, Scan::InCntPos{P_<uint32_t>(c->cnt), P_<uint32_t>(c->vlist)},
+                      Scan::OutCompactList{P_<uint32_t>(c->vlist), P_<uint32_t>(c->dkey),
+                                           P_<uint32_t>(c->ka), P_<uint32_t>(c->va)},
+                      nvis0, sc + 0));
+      CR_TRY(read_u32(c, sc + 0, &nvis));
+    }
     CR_TRACE(c, "compaction");
   }
   CR_CUDA(c, cudaEventRecord(c->ev[1], str));
@@ -646,8 +693,16 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   uint32_t *tA = P_<uint32_t>(c->pta), *pA = P_<uint32_t>(c->pva);
   uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
   if (P > 0) {
-    k_emit<<<grid_for(nvis, 128), 128, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis,
-                                                  P_<float4>(c->mean4), P_<float4>(c->cov8), tA, pA);
+    uint32_t* n_el = sc + 5;
+    CR_CUDA(c, cudaMemsetAsync(n_el, 0, 4, str));
+    k_emit_slots<<<grid_for(nvis, 256), 256, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis,
+                                                       P_<uint4>(c->slots), tA, pA,
+                                                       P_<uint32_t>(c->elist), n_el);
+    CR_LAUNCHED(c);
+    k_emit_groups<<<bin_grid, kBinThreads, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs),
+                                                     P_<uint32_t>(c->elist), n_el, G,
+                                                     P_<float4>(c->mean4), P_<float4>(c->geom),
+                                                     tA, pA);
     CR_LAUNCHED(c);
   }
   CR_TRACE(c, "offsets+emit");

@@ -1,5 +1,5 @@
 // cr_device.cuh — device-side state and exact-arithmetic helpers of the
-// CoherentRaster B200 path.  Included once by cr_all.cu (unity build, so the
+// CoherentRaster B200 path.  Included once by cr_api.cu (unity build, so the
 // __constant__ rig is visible to every kernel without -rdc).
 //
 // Exactness rule (DESIGN.md §3 "exact path"): everything that decides a view
@@ -107,49 +107,51 @@ __device__ __forceinline__ bool cov2d_exact(const CamDev& c, const CamConstDev& 
   return det > 0.0f;
 }
 
-// O7 (AccuTile reading): row range of one view's ellipse {d^T Sigma^-1 d <= tau}.
-struct ViewRows {
-  float mx, my, ex, ey;
-  int ty0, ty1;
+// O7 (AccuTile reading): tiles whose pixel-centre rectangle meets the ellipse
+// {d^T Sigma^-1 d <= tau}.  Per-record constants (view independent: the
+// cluster shares Sigma2D, Eq.6) are evaluated once; x/16 is evaluated as
+// x*0.0625 (both are the correctly rounded x*2^-4: bit-identical).
+struct EllRec {
+  float a, b, c, det, tau;
+  float ex, ey;  // sqrt(tau a), sqrt(tau c): x / y half extents
+  float dyR;     // (b ex)/a: dy of the rightmost point
+  float tc;      // tau c
+  float ic;      // 1/c (rounded once)
 };
-__device__ __forceinline__ ViewRows view_rows(float mx, float my, float a, float c, float tau,
-                                              int TY) {
-  ViewRows v;
-  v.mx = mx;
-  v.my = my;
-  v.ex = xsqrt(xmul(tau, a));
-  v.ey = xsqrt(xmul(tau, c));
-  v.ty0 = clamp_to_int(ceilf(xdiv(xsub(xsub(my, v.ey), 15.5f), 16.0f)), 0.0f, (float)TY);
-  v.ty1 = clamp_to_int(floorf(xdiv(xsub(xadd(my, v.ey), 0.5f), 16.0f)), -1.0f, (float)(TY - 1));
-  return v;
+__device__ __forceinline__ EllRec ell_rec(float a, float b, float c, float det, float tau) {
+  EllRec e;
+  e.a = a; e.b = b; e.c = c; e.det = det; e.tau = tau;
+  e.ex = xsqrt(xmul(tau, a));
+  e.ey = xsqrt(xmul(tau, c));
+  e.dyR = xdiv(xmul(b, e.ex), a);
+  e.tc = xmul(tau, c);
+  e.ic = xdiv(1.0f, c);
+  return e;
 }
-// Tile columns [tx0, tx1] of row ty; false when the row band misses the ellipse.
-__device__ __forceinline__ bool view_row_cols(const ViewRows& v, float a, float b, float c,
-                                              float det, float tau, int ty, int TX, int& tx0,
-                                              int& tx1) {
-  const float dlo = xmax(xsub(xadd(xmul(16.0f, (float)ty), 0.5f), v.my), -v.ey);
-  const float dhi = xmin(xsub(xadd(xmul(16.0f, (float)ty), 15.5f), v.my), v.ey);
+// row range [ty0, ty1] of one view (mean my)
+__device__ __forceinline__ void view_rows(const EllRec& e, float my, int TY, int& ty0, int& ty1) {
+  ty0 = clamp_to_int(ceilf(xmul(xsub(xsub(my, e.ey), 15.5f), 0.0625f)), 0.0f, (float)TY);
+  ty1 = clamp_to_int(floorf(xmul(xsub(xadd(my, e.ey), 0.5f), 0.0625f)), -1.0f, (float)(TY - 1));
+}
+// Tile columns [tx0, tx1] of row ty for one view (mean mx, my); false when
+// the row band misses the ellipse.
+__device__ __forceinline__ bool view_row_cols(const EllRec& e, float mx, float my, int ty, int TX,
+                                              int& tx0, int& tx1) {
+  const float dlo = xmax(xsub(xadd(xmul(16.0f, (float)ty), 0.5f), my), -e.ey);
+  const float dhi = xmin(xsub(xadd(xmul(16.0f, (float)ty), 15.5f), my), e.ey);
   if (dlo > dhi) return false;
-  const float dyR = xdiv(xmul(b, v.ex), a);
-  const float dyL = -dyR;
-  const float tc = xmul(tau, c);
-  const float hlo = xsqrt(xmax(0.0f, xmul(det, xsub(tc, xmul(dlo, dlo)))));
-  const float hhi = xsqrt(xmax(0.0f, xmul(det, xsub(tc, xmul(dhi, dhi)))));
-  float right, left;
-  if (dlo <= dyR && dyR <= dhi) {
-    right = v.ex;
-  } else {
-    right = xmax(xdiv(xadd(xmul(b, dlo), hlo), c), xdiv(xadd(xmul(b, dhi), hhi), c));
-  }
-  if (dlo <= dyL && dyL <= dhi) {
-    left = -v.ex;
-  } else {
-    left = xmin(xdiv(xsub(xmul(b, dlo), hlo), c), xdiv(xsub(xmul(b, dhi), hhi), c));
-  }
-  right = xadd(v.mx, right);
-  left = xadd(v.mx, left);
-  tx0 = clamp_to_int(ceilf(xdiv(xsub(left, 15.5f), 16.0f)), 0.0f, (float)TX);
-  tx1 = clamp_to_int(floorf(xdiv(xsub(right, 0.5f), 16.0f)), -1.0f, (float)(TX - 1));
+  const float dyR = e.dyR, dyL = -e.dyR;
+  const float hlo = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dlo, dlo)))));
+  const float hhi = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dhi, dhi)))));
+  const float bl = xmul(e.b, dlo), bh = xmul(e.b, dhi);
+  const float right = (dlo <= dyR && dyR <= dhi)
+                          ? e.ex
+                          : xmax(xmul(xadd(bl, hlo), e.ic), xmul(xadd(bh, hhi), e.ic));
+  const float left = (dlo <= dyL && dyL <= dhi)
+                         ? -e.ex
+                         : xmin(xmul(xsub(bl, hlo), e.ic), xmul(xsub(bh, hhi), e.ic));
+  tx0 = clamp_to_int(ceilf(xmul(xsub(xadd(mx, left), 15.5f), 0.0625f)), 0.0f, (float)TX);
+  tx1 = clamp_to_int(floorf(xmul(xsub(xadd(mx, right), 0.5f), 0.0625f)), -1.0f, (float)(TX - 1));
   return true;
 }
 

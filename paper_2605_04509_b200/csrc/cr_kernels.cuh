@@ -188,69 +188,108 @@ __global__ void k_upload(long long M, int nc3, const float* __restrict__ means,
 }
 
 // ===========================================================================
-// O8 — cluster tile union (Alg.2 GenerateKeys, P:791-808) restricted to the
-// band rows.  EMIT=false counts; EMIT=true writes tile ids (ascending within
-// each row, rows ascending) + payload r.  Identical set on both passes: the
-// same inputs go through the same exactly-rounded code.
+// Cameras staged in shared memory (stride 17 floats: the <= 32 distinct views
+// read by one warp hit distinct banks).
 // ===========================================================================
-template <bool EMIT>
-__device__ uint32_t tile_union(int k, float mux, float muy, float muz, float a, float b, float c,
-                               float det, float tau, uint32_t* __restrict__ out_t,
-                               uint32_t* __restrict__ out_v, uint32_t payload) {
-  const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
-  const int j0 = k * s;
-  const int nv = min(j0 + s, N) - j0;
-  float vmx[kMaxCluster], vmy[kMaxCluster];
-  int vrow[kMaxCluster];  // ty0 | ty1 << 16 as 16-bit fields; ty0 = -1 marks an invisible view
-  float ex = 0.f, ey = 0.f;
-  int rmin = TY, rmax = -1;
-  for (int l = 0; l < nv; ++l) {
-    const CamDev& cam = c_cams[j0 + l];
-    const F3 p = cam_point_exact(cam, mux, muy, muz);
-    if (!(p.z >= c_fp.znear)) {  // Z12: this view contributes no tiles
-      vrow[l] = 0x0000FFFF;      // ty0 = -1 (never produced for a visible view)
-      continue;
-    }
-    float mx, my;
-    mean2d_exact(cam, p, mx, my);
-    const ViewRows vr = view_rows(mx, my, a, c, tau, TY);
-    ex = vr.ex;
-    ey = vr.ey;
-    vmx[l] = mx;
-    vmy[l] = my;
-    vrow[l] = (vr.ty0 & 0xFFFF) | ((vr.ty1 & 0xFFFF) << 16);
-    rmin = min(rmin, vr.ty0);
-    rmax = max(rmax, vr.ty1);
+constexpr int kCamStride = 17;
+__device__ __forceinline__ void stage_cams(float* s_cam) {
+  const int N = c_fp.N;
+  for (int q = threadIdx.x; q < N * 16; q += blockDim.x) {
+    const int j = q >> 4, f = q & 15;
+    s_cam[j * kCamStride + f] = (&c_cams[j].R[0])[f];
   }
-  rmin = max(rmin, c_fp.row0);
-  rmax = min(rmax, c_fp.row1 - 1);
-  uint32_t n = 0;
-  int iv[kMaxCluster];
-  for (int ty = rmin; ty <= rmax; ++ty) {
-    int lo = 0x7fffffff, hi = -1, ni = 0;
-    for (int l = 0; l < nv; ++l) {
-      const int ty0 = (int)(short)(vrow[l] & 0xFFFF), ty1 = (int)(short)(vrow[l] >> 16);
-      if (ty0 < 0 || ty < ty0 || ty > ty1) continue;  // invisible view or row outside
-      ViewRows vr;
-      vr.mx = vmx[l]; vr.my = vmy[l]; vr.ex = ex; vr.ey = ey;
-      int tx0, tx1;
-      if (!view_row_cols(vr, a, b, c, det, tau, ty, TX, tx0, tx1)) continue;
-      if (tx0 > tx1) continue;
-      iv[ni++] = tx0 | (tx1 << 16);
-      lo = min(lo, tx0);
-      hi = max(hi, tx1);
+}
+__device__ __forceinline__ CamDev load_cam(const float* s_cam, int j) {
+  CamDev c;
+  const float* p = s_cam + j * kCamStride;
+#pragma unroll
+  for (int f = 0; f < 9; ++f) c.R[f] = p[f];
+  c.t[0] = p[9]; c.t[1] = p[10]; c.t[2] = p[11];
+  c.fx = p[12]; c.fy = p[13]; c.cx = p[14]; c.cy = p[15];
+  return c;
+}
+
+// Group-of-G-lane reductions (G a power of two, groups aligned in the warp).
+// Every caller keeps the WHOLE warp converged (warp-uniform loops), so the
+// shuffles use the full mask and stay inside the group via offsets < G.
+__device__ __forceinline__ int gmin(int v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int gmax(int v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ unsigned long long gor64(unsigned long long v, int G) {
+  for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ===========================================================================
+// O8 — cluster tile union (Alg.2 GenerateKeys, P:791-808) restricted to the
+// band rows, computed by a GROUP of G lanes: lane v of the group owns view
+// j = k*s + v of cluster k (exact per-view mean, Eq.5, and AccuTile rows /
+// per-row columns, O7); per tile row the views' column intervals are merged
+// by shuffles into a 64-bit mask (or, for spans >= 64 tiles, a per-column
+// ballot).  Identical set on every call: same inputs, same exactly-rounded
+// code.  MODE 0 counts; MODE 1 also fills a 32-byte "union slot" (rows of
+// <= 32-tile masks, see k_emit_slots) for the emit pass; MODE 2 writes the
+// tile ids (rows ascending, columns ascending) + payload r.
+// Must be called by all 32 lanes of the warp (inactive groups: active=false).
+// ===========================================================================
+constexpr int kSlotRows = 4;
+constexpr uint32_t kSlotOverflow = 0x80000000u;
+
+template <int MODE>
+__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, int G,
+                                unsigned gm, float mux, float muy, float muz, const EllRec& el,
+                                uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
+                                uint32_t payload, uint4* __restrict__ slot) {
+  const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
+  const int j = k * s + v;
+  bool vis = false;
+  float mx = 0.f, my = 0.f;
+  int ty0 = 0x7fffffff, ty1 = -1;
+  if (active && v < s && j < N) {
+    const CamDev cam = load_cam(s_cam, j);
+    const F3 p = cam_point_exact(cam, mux, muy, muz);
+    if (p.z >= c_fp.znear) {  // Z12: a view that cannot see i contributes no tiles
+      mean2d_exact(cam, p, mx, my);
+      view_rows(el, my, TY, ty0, ty1);
+      vis = true;
     }
-    if (ni == 0) continue;
-    const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
-    if (hi - lo < 64) {
-      unsigned long long mask = 0ull;
-      for (int q = 0; q < ni; ++q) {
-        const int s0 = iv[q] & 0xFFFF, s1 = iv[q] >> 16;
-        const int len = s1 - s0 + 1;
-        const unsigned long long bits = (len >= 64) ? ~0ull : ((1ull << len) - 1ull);
-        mask |= bits << (s0 - lo);
+  }
+  const int rmin = max(gmin(vis ? ty0 : 0x7fffffff, G), c_fp.row0);
+  const int rmax = min(gmax(vis ? ty1 : -1, G), c_fp.row1 - 1);
+  const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
+  const int it_max = __reduce_max_sync(0xffffffffu, nrows);
+  const bool lead = (threadIdx.x & (G - 1)) == 0;
+  uint32_t n = 0;
+  uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // slot words (MODE 1)
+  bool ovf = nrows > kSlotRows;
+  for (int it = 0; it < it_max; ++it) {
+    const int ty = rmin + it;
+    const bool rowok = it < nrows;
+    int tx0 = 0x7fffffff, tx1 = -1;
+    if (rowok && vis && ty >= ty0 && ty <= ty1) {
+      int q0, q1;
+      if (view_row_cols(el, mx, my, ty, TX, q0, q1) && q0 <= q1) {
+        tx0 = q0;
+        tx1 = q1;
       }
-      if (EMIT) {
+    }
+    const int lo = gmin(tx0, G), hi = gmax(tx1, G);
+    const bool any = rowok && hi >= lo;
+    const bool narrow = any && hi - lo < 64;
+    const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
+    unsigned long long mask = 0ull;
+    if (narrow && tx1 >= tx0) {
+      const int len = tx1 - tx0 + 1;
+      mask = ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - lo);
+    }
+    mask = gor64(mask, G);
+    if (narrow) {
+      if (MODE == 2 && lead) {
         unsigned long long m = mask;
         uint32_t q = n;
         while (m) {
@@ -262,32 +301,51 @@ __device__ uint32_t tile_union(int k, float mux, float muy, float muz, float a, 
         }
       }
       n += (uint32_t)__popcll(mask);
-    } else {
-      for (int tx = lo; tx <= hi; ++tx) {
-        bool hit = false;
-        for (int q = 0; q < ni; ++q) hit |= ((iv[q] & 0xFFFF) <= tx && tx <= (iv[q] >> 16));
-        if (hit) {
-          if (EMIT) {
-            out_t[n] = rowbase + (uint32_t)tx;
-            out_v[n] = payload;
+    }
+    if (MODE == 1 && rowok && it < kSlotRows) {
+      if (any && !(narrow && hi - lo < 32)) ovf = true;
+      if (narrow && hi - lo < 32) {
+#pragma unroll
+        for (int q = 0; q < kSlotRows; ++q)
+          if (q == it) {
+            sw[1 + (q >> 1)] |= (uint32_t)lo << ((q & 1) * 16);
+            sw[4 + q] = (uint32_t)mask;
           }
-          ++n;
-        }
       }
     }
+    // wide rows (>= 64 tiles): per-column ballot, warp-uniform trip count
+    const int span = (any && !narrow) ? hi - lo + 1 : 0;
+    const int smax = __reduce_max_sync(0xffffffffu, span);
+    for (int q = 0; q < smax; ++q) {
+      const int tx = lo + q;
+      const unsigned bal = __ballot_sync(0xffffffffu, q < span && tx0 <= tx && tx <= tx1);
+      if (q < span && (bal & gm) != 0u) {
+        if (MODE == 2 && lead) {
+          out_t[n] = rowbase + (uint32_t)tx;
+          out_v[n] = payload;
+        }
+        ++n;
+      }
+    }
+  }
+  if (MODE == 1 && active && lead) {
+    sw[0] = (uint32_t)(rmin & 0xFFFF) | ((uint32_t)min(nrows, kSlotRows) << 16) |
+            (ovf ? kSlotOverflow : 0u);
+    sw[3] = n;
+    slot[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+    slot[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
   }
   return n;
 }
 
 // ===========================================================================
-// a4 — Preprocess + SH (Cross-view Coherent Attribute Reuse, Eq.6)
-// fused with the tile-union count (a6).  One thread per Gaussian, looping
-// over the K clusters so the SH coefficients are read once and evaluated K
-// times.  Writes per (k,i) (index r = k*M + i, k-major):
+// a4 — Preprocess + SH (Cross-view Coherent Attribute Reuse, Eq.6).
+// One thread per Gaussian, looping over the K clusters so the SH
+// coefficients are read once and evaluated K times.  Per (k,i), r = k*M + i:
 //   rec0[r] = (A', B', C', log2 o)  conic prescaled by -log2(e)/2, -log2(e)
 //   rec1[r] = (r, g, b, depth)      colour at v'_k, depth d_{i,k}
-//   cnt[r]  = |T_{i,k}| in the band (0 if culled)
-//   dkey[r] = bits(d_{i,k})
+//   geom[r] = (a, b, c, det)        exact EWA Sigma2D for the tile test (O6/O7)
+//   dkey[r] = bits(d_{i,k}),  vis[r] = 1 if (i,k) survives culling, else 0
 // ===========================================================================
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -295,7 +353,7 @@ template <int DEG>
 __global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
     const float* __restrict__ shsoa, float4* __restrict__ rec0, float4* __restrict__ rec1,
-    uint32_t* __restrict__ cnt, uint32_t* __restrict__ dkey,
+    float4* __restrict__ geom, uint32_t* __restrict__ dkey, uint32_t* __restrict__ vis,
     unsigned long long* __restrict__ counters /* near, degenerate, opacity */) {
   constexpr int NC = (DEG + 1) * (DEG + 1);
   const long long M = c_fp.M;
@@ -307,61 +365,64 @@ __global__ void __launch_bounds__(128) k_preprocess(
     const float4 ca = cov8[2 * i], cb = cov8[2 * i + 1];
     const float S6[6] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y};
     const float o = cb.z;
-    float sh[NC][3];
-#pragma unroll
-    for (int q = 0; q < NC; ++q)
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) sh[q][ch] = shsoa[(long long)(q * 3 + ch) * M + i];
     const float lo2 = log2f(o);
     const int K = c_fp.K;
-    if (!(tau > 0.0f)) n_op = 1;
-    for (int k = 0; k < K; ++k) {
-      const long long r = (long long)k * M + i;
-      if (!(tau > 0.0f)) { cnt[r] = 0; continue; }
-      const int jr = c_rep[k];
-      const CamDev& rc = c_cams[jr];
-      const F3 p = cam_point_exact(rc, m.x, m.y, m.z);
-      if (p.z < c_fp.znear) { cnt[r] = 0; ++n_near; continue; }
-      float a, b, c, det;
-      if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { cnt[r] = 0; ++n_deg; continue; }
-      // conic (tolerance path), prescaled for exp2
-      const float A = c / det, B = -b / det, C = a / det;
-      rec0[r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
-      // SH colour at the representative camera centre (O11)
-      const CamConstDev& cc = c_ccon[jr];
-      float dx = m.x - cc.C[0], dy = m.y - cc.C[1], dz = m.z - cc.C[2];
-      const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-      dx *= inv; dy *= inv; dz *= inv;
-      float col[3];
+    if (!(tau > 0.0f)) {
+      n_op = 1;
+      for (int k = 0; k < K; ++k) vis[(long long)k * M + i] = 0;
+    } else {
+      float sh[NC][3];
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float v = 0.28209479177387814f * sh[0][ch];
-        if (DEG >= 1) {
-          v += -0.4886025119029199f * dy * sh[1][ch] + 0.4886025119029199f * dz * sh[2][ch] -
-               0.4886025119029199f * dx * sh[3][ch];
-        }
-        if (DEG >= 2) {
-          const float xx = dx * dx, yy = dy * dy, zz = dz * dz;
-          v += 1.0925484305920792f * dx * dy * sh[4][ch] +
-               -1.0925484305920792f * dy * dz * sh[5][ch] +
-               0.31539156525252005f * (2.f * zz - xx - yy) * sh[6][ch] +
-               -1.0925484305920792f * dx * dz * sh[7][ch] +
-               0.5462742152960396f * (xx - yy) * sh[8][ch];
-          if (DEG >= 3) {
-            v += -0.5900435899266435f * dy * (3.f * xx - yy) * sh[9][ch] +
-                 2.890611442640554f * dx * dy * dz * sh[10][ch] +
-                 -0.4570457994644658f * dy * (4.f * zz - xx - yy) * sh[11][ch] +
-                 0.3731763325901154f * dz * (2.f * zz - 3.f * xx - 3.f * yy) * sh[12][ch] +
-                 -0.4570457994644658f * dx * (4.f * zz - xx - yy) * sh[13][ch] +
-                 1.445305721320277f * dz * (xx - yy) * sh[14][ch] +
-                 -0.5900435899266435f * dx * (xx - 3.f * yy) * sh[15][ch];
+      for (int q = 0; q < NC; ++q)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) sh[q][ch] = shsoa[(long long)(q * 3 + ch) * M + i];
+      for (int k = 0; k < K; ++k) {
+        const long long r = (long long)k * M + i;
+        const int jr = c_rep[k];
+        const CamDev& rc = c_cams[jr];
+        const F3 p = cam_point_exact(rc, m.x, m.y, m.z);
+        if (p.z < c_fp.znear) { vis[r] = 0; ++n_near; continue; }
+        float a, b, c, det;
+        if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { vis[r] = 0; ++n_deg; continue; }
+        vis[r] = 1;
+        geom[r] = make_float4(a, b, c, det);
+        const float A = c / det, B = -b / det, C = a / det;  // conic (tolerance path)
+        rec0[r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
+        // SH colour at the representative camera centre (O11)
+        const CamConstDev& cc = c_ccon[jr];
+        float dx = m.x - cc.C[0], dy = m.y - cc.C[1], dz = m.z - cc.C[2];
+        const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+        dx *= inv; dy *= inv; dz *= inv;
+        float col[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          float v = 0.28209479177387814f * sh[0][ch];
+          if (DEG >= 1) {
+            v += -0.4886025119029199f * dy * sh[1][ch] + 0.4886025119029199f * dz * sh[2][ch] -
+                 0.4886025119029199f * dx * sh[3][ch];
           }
+          if (DEG >= 2) {
+            const float xx = dx * dx, yy = dy * dy, zz = dz * dz;
+            v += 1.0925484305920792f * dx * dy * sh[4][ch] +
+                 -1.0925484305920792f * dy * dz * sh[5][ch] +
+                 0.31539156525252005f * (2.f * zz - xx - yy) * sh[6][ch] +
+                 -1.0925484305920792f * dx * dz * sh[7][ch] +
+                 0.5462742152960396f * (xx - yy) * sh[8][ch];
+            if (DEG >= 3) {
+              v += -0.5900435899266435f * dy * (3.f * xx - yy) * sh[9][ch] +
+                   2.890611442640554f * dx * dy * dz * sh[10][ch] +
+                   -0.4570457994644658f * dy * (4.f * zz - xx - yy) * sh[11][ch] +
+                   0.3731763325901154f * dz * (2.f * zz - 3.f * xx - 3.f * yy) * sh[12][ch] +
+                   -0.4570457994644658f * dx * (4.f * zz - xx - yy) * sh[13][ch] +
+                   1.445305721320277f * dz * (xx - yy) * sh[14][ch] +
+                   -0.5900435899266435f * dx * (xx - 3.f * yy) * sh[15][ch];
+            }
+          }
+          col[ch] = fmaxf(v + 0.5f, 0.0f);
         }
-        col[ch] = fmaxf(v + 0.5f, 0.0f);
+        rec1[r] = make_float4(col[0], col[1], col[2], p.z);
+        dkey[r] = __float_as_uint(p.z);
       }
-      rec1[r] = make_float4(col[0], col[1], col[2], p.z);
-      dkey[r] = __float_as_uint(p.z);
-      cnt[r] = tile_union<false>(k, m.x, m.y, m.z, a, b, c, det, tau, nullptr, nullptr, 0);
     }
   }
   // block-aggregated culling counters
@@ -376,30 +437,123 @@ __global__ void __launch_bounds__(128) k_preprocess(
 }
 
 // ===========================================================================
-// a6 emit — one thread per depth-sorted visible record e: recompute Sigma2D
-// at v'_k and the cluster tile union, write <tile, r> at offs[e].
+// a6 count — one G-lane group per visible record (list `recs`, n entries):
+// cnt[r] = |T_{i,k}| in the band.  Grid-stride (persistent) so the camera
+// table is staged in shared memory once per CTA.
 // ===========================================================================
-__global__ void __launch_bounds__(128) k_emit(const uint32_t* __restrict__ rec_sorted,
-                                              const uint32_t* __restrict__ offs, uint32_t nrec,
-                                              const float4* __restrict__ mean4,
-                                              const float4* __restrict__ cov8,
-                                              uint32_t* __restrict__ out_t,
-                                              uint32_t* __restrict__ out_v) {
+constexpr int kBinThreads = 256;
+
+__global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
+                                                       uint32_t n, int G,
+                                                       const float4* __restrict__ mean4,
+                                                       const float4* __restrict__ geom,
+                                                       uint32_t* __restrict__ cnt,
+                                                       uint4* __restrict__ slots) {
+  __shared__ float s_cam[kMaxViews * kCamStride];
+  stage_cams(s_cam);
+  __syncthreads();
+  const unsigned long long M = (unsigned long long)c_fp.M;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1);
+  const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int gpw = 32 / G;  // groups per warp
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * (kBinThreads / 32);
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * gpw;
+       wb < n; wb += nwarps * gpw) {  // warp-uniform loop
+    const unsigned long long g = wb + lane / G;
+    const bool active = g < n;
+    uint32_t r = 0;
+    float4 m = make_float4(0.f, 0.f, 0.f, 1.f), q = make_float4(1.f, 0.f, 1.f, 1.f);
+    int k = 0;
+    if (active) {
+      r = recs[g];
+      k = (int)(r / M);
+      m = mean4[(long long)r - (long long)k * (long long)M];
+      q = geom[r];
+    }
+    const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
+    const uint32_t c = group_union<1>(s_cam, active, k, v, G, gm, m.x, m.y, m.z, el, nullptr,
+                                      nullptr, 0, slots + 2ull * r);
+    if (active && v == 0) cnt[r] = c;
+  }
+}
+
+// ===========================================================================
+// a6 emit, fast path — one thread per depth-sorted record e decodes the union
+// slot written by k_count and writes <tile, r> at offs[e].  Records whose
+// union did not fit a slot (> 4 rows or a row >= 32 tiles) are appended to
+// `elist` for k_emit_groups.
+// ===========================================================================
+__global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__ rec_sorted,
+                                                    const uint32_t* __restrict__ offs, uint32_t n,
+                                                    const uint4* __restrict__ slots,
+                                                    uint32_t* __restrict__ out_t,
+                                                    uint32_t* __restrict__ out_v,
+                                                    uint32_t* __restrict__ elist,
+                                                    uint32_t* __restrict__ n_elist) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nrec) return;
+  if (e >= n) return;
   const uint32_t r = rec_sorted[e];
-  const long long M = c_fp.M;
-  const int k = (int)(r / (unsigned long long)M);
-  const long long i = (long long)r - (long long)k * M;
-  const float4 m = mean4[i];
-  const float4 ca = cov8[2 * i], cb = cov8[2 * i + 1];
-  const float S6[6] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y};
-  const int jr = c_rep[k];
-  const F3 p = cam_point_exact(c_cams[jr], m.x, m.y, m.z);
-  float a, b, c, det;
-  cov2d_exact(c_cams[jr], c_ccon[jr], p, S6, a, b, c, det);
-  const uint32_t o = offs[e];
-  tile_union<true>(k, m.x, m.y, m.z, a, b, c, det, m.w, out_t + o, out_v + o, r);
+  const uint4 h = slots[2ull * r];
+  if (h.x & kSlotOverflow) {
+    elist[atomicAdd(n_elist, 1u)] = e;
+    return;
+  }
+  const uint4 mk = slots[2ull * r + 1];
+  const uint32_t row0 = h.x & 0xFFFF, nrows = (h.x >> 16) & 7;
+  const uint32_t TX = (uint32_t)c_fp.TX;
+  const uint32_t lo[4] = {h.y & 0xFFFF, h.y >> 16, h.z & 0xFFFF, h.z >> 16};
+  const uint32_t ms[4] = {mk.x, mk.y, mk.z, mk.w};
+  uint32_t o = offs[e];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if ((uint32_t)q >= nrows) break;
+    uint32_t m = ms[q];
+    const uint32_t base = (row0 + q) * TX + lo[q];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      out_t[o] = base + bit;
+      out_v[o] = r;
+      ++o;
+    }
+  }
+}
+
+// a6 emit, general path — one G-lane group per listed sorted position e
+// (recomputes the union; n read on the device).
+__global__ void __launch_bounds__(kBinThreads) k_emit_groups(
+    const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
+    const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr, int G,
+    const float4* __restrict__ mean4, const float4* __restrict__ geom,
+    uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
+  __shared__ float s_cam[kMaxViews * kCamStride];
+  stage_cams(s_cam);
+  __syncthreads();
+  const uint32_t n = *n_ptr;
+  const unsigned long long M = (unsigned long long)c_fp.M;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1);
+  const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int gpw = 32 / G;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * (kBinThreads / 32);
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * gpw;
+       wb < n; wb += nwarps * gpw) {
+    const unsigned long long g = wb + lane / G;
+    const bool active = g < n;
+    uint32_t r = 0, o = 0;
+    float4 m = make_float4(0.f, 0.f, 0.f, 1.f), q = make_float4(1.f, 0.f, 1.f, 1.f);
+    int k = 0;
+    if (active) {
+      const uint32_t e = elist ? elist[g] : (uint32_t)g;
+      r = rec_sorted[e];
+      k = (int)(r / M);
+      m = mean4[(long long)r - (long long)k * (long long)M];
+      q = geom[r];
+      o = offs[e];
+    }
+    const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
+    group_union<2>(s_cam, active, k, v, G, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r,
+                   nullptr);
+  }
 }
 
 // ===========================================================================

@@ -127,7 +127,7 @@ class CoherentRaster:
         W, H = self.display["width"], self.display["height"]
         r0, r1 = rows if rows else (0, self.TY)
         y0, y1 = r0 * 16, min(H, r1 * 16)
-        return (y1 - y0, W, 3)
+        return (max(0, y1 - y0), W, 3)
 
     def render(self, cluster_size: int = 8, remap: bool = True, kernel: int | None = None,
                background=(0.0, 0.0, 0.0), output_format: str = "rgb8", rows=None, out=None,
