@@ -643,9 +643,19 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     CR_TRY(read_u32(c, sc + 4, &nvis0));
     CR_CUDA(c, cudaMemsetAsync(c->cnt.p, 0, (size_t)R * 4, str));
     if (nvis0 > 0) {
-      k_count<<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0, G,
-                                                 P_<float4>(c->mean4), P_<float4>(c->geom),
-                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots));
+#define CR_COUNT(GG)                                                                        \
+  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0,             \
+                                                 P_<float4>(c->mean4), P_<float4>(c->geom), \
+                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots))
+      switch (G) {
+        case 1: CR_COUNT(1); break;
+        case 2: CR_COUNT(2); break;
+        case 4: CR_COUNT(4); break;
+        case 8: CR_COUNT(8); break;
+        case 16: CR_COUNT(16); break;
+        default: CR_COUNT(32); break;
+      }
+#undef CR_COUNT
       CR_LAUNCHED(c);
       CR_TRACE(c, "count");
       // records with >= 1 tile in the band -> (depth key, r)
@@ -699,10 +709,19 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
                                                        P_<uint4>(c->slots), tA, pA,
                                                        P_<uint32_t>(c->elist), n_el);
     CR_LAUNCHED(c);
-    k_emit_groups<<<bin_grid, kBinThreads, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs),
-                                                     P_<uint32_t>(c->elist), n_el, G,
-                                                     P_<float4>(c->mean4), P_<float4>(c->geom),
-                                                     tA, pA);
+#define CR_EMITG(GG)                                                                        \
+  k_emit_groups<GG><<<bin_grid, kBinThreads, 0, str>>>(                                     \
+      rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->elist), n_el, P_<float4>(c->mean4), \
+      P_<float4>(c->geom), tA, pA)
+    switch (G) {
+      case 1: CR_EMITG(1); break;
+      case 2: CR_EMITG(2); break;
+      case 4: CR_EMITG(4); break;
+      case 8: CR_EMITG(8); break;
+      case 16: CR_EMITG(16); break;
+      default: CR_EMITG(32); break;
+    }
+#undef CR_EMITG
     CR_LAUNCHED(c);
   }
   CR_TRACE(c, "offsets+emit");

@@ -6,15 +6,20 @@
 //   consecutive Psi ranks of one cluster k) from a shared-memory queue.  Per
 //   chunk the warp streams list (t,k) in 32-entry batches: lane l gathers
 //   entry l's record and world mean once, projects the mean for each of the
-//   <= 8 distinct views present in the chunk (per-view mu2D_{i,j}, Eq.5), and
-//   stages everything in shared memory; then every lane walks the batch from
-//   shared memory (broadcast reads) for its own subpixel.  A warp ballot ends
-//   the list as soon as every lane has saturated.  Results go to a smem tile
-//   and leave in coalesced row stores.
+//   <= 8 distinct views present in the chunk (per-view mu2D_{i,j}, Eq.5),
+//   stages everything in shared memory and ballots, per view, which entries
+//   can reach that view's subpixels at all (alpha >= 1/255 box test: the
+//   cluster tile union holds many entries a given view never touches,
+//   P:379-382, and skipping them is exact).  Every lane then walks only its
+//   view's surviving entries from shared memory (broadcast reads).  A warp
+//   ballot ends the list as soon as every lane has saturated.  Results go to
+//   a smem tile and leave in coalesced row stores.
 // k_composite_thread (the paper's design): one thread per subpixel rank r,
 //   x = Psi(r) (remap=1) or raster order (remap=0), private list traversal
 //   with direct gathers and a direct scattered store.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "cr_device.cuh"
 
 namespace cr {
@@ -90,6 +95,28 @@ __device__ __forceinline__ void add_evals(unsigned long long* evals, unsigned lo
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(evals, n);
 }
 
+struct Staged {  // one list entry as gathered by one lane
+  float4 m, r0, r1;
+  bool valid;
+};
+__device__ __forceinline__ Staged gather_entry(const float4* __restrict__ rec0,
+                                               const float4* __restrict__ rec1,
+                                               const float4* __restrict__ mean4, uint32_t r,
+                                               bool valid, long long kM) {
+  Staged st;
+  st.valid = valid;
+  if (valid) {
+    st.m = mean4[(long long)r - kM];
+    st.r0 = rec0[r];
+    st.r1 = rec1[r];
+  } else {
+    st.m = make_float4(0.f, 0.f, 0.f, 0.f);
+    st.r0 = st.m;
+    st.r1 = st.m;
+  }
+  return st;
+}
+
 template <int FMT, bool COUNT>
 __global__ void __launch_bounds__(kCompWarps * 32) k_composite_staged(
     const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,
@@ -101,6 +128,7 @@ __global__ void __launch_bounds__(kCompWarps * 32) k_composite_staged(
   __shared__ float4 s_rec[kCompWarps][32];
   __shared__ float4 s_col[kCompWarps][32];
   __shared__ float2 s_mu[kCompWarps][kSlots][32];
+  __shared__ float4 s_box[kCompWarps][kSlots];  // per staged view: pixel box centre, half size
   __shared__ float s_out[kTileSub];
   __shared__ int s_next;
   const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
@@ -122,18 +150,17 @@ __global__ void __launch_bounds__(kCompWarps * 32) k_composite_staged(
     const uint32_t ch = ch_t[c];
     const int start = ch & 1023, len = ((ch >> 10) & 63) + 1, k = ch >> 16;
     // this lane's subpixel
-    int l = 0, u = 0, j = 0;
-    float px = 0.f, py = 0.f;
+    int l = 0, u = 0, j = 0, x = 0, y = 0;
     const bool mine = lane < len;
     if (mine) {
       l = ps[start + lane];
       const int ly = l / 48, rem = l % 48, lx = rem / 3;
       u = rem % 3;
-      const int x = tx * 16 + lx, y = ty * 16 + ly;
+      x = tx * 16 + lx;
+      y = ty * 16 + ly;
       j = V[((long long)y * W + x) * 3 + u];
-      px = (float)x + 0.5f;
-      py = (float)y + 0.5f;
     }
+    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
     const int jlo = __shfl_sync(0xffffffffu, j, 0);
     const int jhi = __shfl_sync(0xffffffffu, j, len - 1);
     const int nsl = jhi - jlo + 1;
@@ -144,32 +171,66 @@ __global__ void __launch_bounds__(kCompWarps * 32) k_composite_staged(
       const bool active = mine && slot >= g0 && slot < g0 + kSlots;
       if (!__any_sync(0xffffffffu, active)) continue;
       const int ns = min(kSlots, nsl - g0);
+      const int sl = slot - g0;
+      // pixel-centre box of each staged view's subpixels (for the per-view cull)
+      for (int v = 0; v < ns; ++v) {
+        const bool in = active && sl == v;
+        const int x0 = __reduce_min_sync(0xffffffffu, in ? x : 0x7fffffff);
+        const int x1 = __reduce_max_sync(0xffffffffu, in ? x : -0x7fffffff);
+        const int y0 = __reduce_min_sync(0xffffffffu, in ? y : 0x7fffffff);
+        const int y1 = __reduce_max_sync(0xffffffffu, in ? y : -0x7fffffff);
+        if (lane == 0)
+          s_box[w][v] = make_float4(0.5f * (float)(x0 + x1) + 0.5f, 0.5f * (float)(y0 + y1) + 0.5f,
+                                    0.5f * (float)(x1 - x0), 0.5f * (float)(y1 - y0));
+      }
+      __syncwarp();
       float T = 1.0f, C = 0.0f;
       bool done = !active;
+      // two-stage software pipeline: records of batch b+32 and indices of
+      // batch b+64 are in flight while batch b is blended
+      uint32_t r_nxt = (e0 + 32 + lane < e1) ? vals[e0 + 32 + lane] : 0u;
+      Staged cur = gather_entry(rec0, rec1, mean4, (e0 + lane < e1) ? vals[e0 + lane] : 0u,
+                                e0 + lane < e1, kM);
       for (uint32_t b = e0; b < e1; b += 32) {
-        const uint32_t e = b + lane;
-        if (e < e1) {
-          const uint32_t r = vals[e];
-          const float4 m = mean4[(long long)r - kM];
-          s_rec[w][lane] = rec0[r];
-          s_col[w][lane] = rec1[r];
-          for (int v = 0; v < ns; ++v) s_mu[w][v][lane] = mean2d_fast(c_cams[jlo + g0 + v], m.x, m.y, m.z);
+        const Staged nxt = gather_entry(rec0, rec1, mean4, r_nxt, b + 32 + lane < e1, kM);
+        r_nxt = (b + 64 + lane < e1) ? vals[b + 64 + lane] : 0u;
+        float hx = -1.f, hy = -1.f;
+        if (cur.valid) {
+          s_rec[w][lane] = cur.r0;
+          s_col[w][lane] = cur.r1;
+          const __half2 ext = *reinterpret_cast<const __half2*>(&cur.r1.w);
+          hx = __low2float(ext);
+          hy = __high2float(ext);
+        }
+        unsigned mymask = 0u;
+        for (int v = 0; v < ns; ++v) {
+          const float2 mu = mean2d_fast(c_cams[jlo + g0 + v], cur.m.x, cur.m.y, cur.m.z);
+          s_mu[w][v][lane] = mu;
+          const float4 bx = s_box[w][v];
+          const bool pass = cur.valid && fabsf(mu.x - bx.x) <= bx.z + hx &&
+                            fabsf(mu.y - bx.y) <= bx.w + hy;
+          const unsigned bits = __ballot_sync(0xffffffffu, pass);
+          if (sl == v) mymask = bits;
         }
         __syncwarp();
         const int n = min(32u, e1 - b);
         if (!done) {
-          const int sl = slot - g0;
-          for (int q = 0; q < n; ++q) {
+          unsigned mm = mymask;
+          int qstop = -1;
+          while (mm) {
+            const int q = __ffs(mm) - 1;
+            mm &= mm - 1;
             const float4 g = s_rec[w][q];
             const float2 mu = s_mu[w][sl][q];
             const float col = (&s_col[w][q].x)[u];
             blend_step(g, mu, col, px, py, T, C, done);
-            if (COUNT) ++nev;
-            if (done) break;
+            if (done) { qstop = q; break; }
           }
+          if (COUNT) nev += (qstop >= 0) ? (unsigned)(qstop + 1) : (unsigned)n;
         }
         if (__all_sync(0xffffffffu, done)) break;
         __syncwarp();
+        cur = nxt;
       }
       __syncwarp();
       if (active) s_out[l] = C + c_fp.bg[u] * T;

@@ -2,6 +2,8 @@
 // range kernels of the CoherentRaster B200 path.  See DESIGN.md §5 for the
 // roofline of each kernel and its algorithmic bytes per unit.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "cr_device.cuh"
 
 namespace cr {
@@ -212,15 +214,21 @@ __device__ __forceinline__ CamDev load_cam(const float* s_cam, int j) {
 // Group-of-G-lane reductions (G a power of two, groups aligned in the warp).
 // Every caller keeps the WHOLE warp converged (warp-uniform loops), so the
 // shuffles use the full mask and stay inside the group via offsets < G.
-__device__ __forceinline__ int gmin(int v, int G) {
+template <int G>
+__device__ __forceinline__ int gmin(int v) {
+#pragma unroll
   for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-__device__ __forceinline__ int gmax(int v, int G) {
+template <int G>
+__device__ __forceinline__ int gmax(int v) {
+#pragma unroll
   for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-__device__ __forceinline__ unsigned long long gor64(unsigned long long v, int G) {
+template <int G>
+__device__ __forceinline__ unsigned long long gor64(unsigned long long v) {
+#pragma unroll
   for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
@@ -240,9 +248,8 @@ __device__ __forceinline__ unsigned long long gor64(unsigned long long v, int G)
 constexpr int kSlotRows = 4;
 constexpr uint32_t kSlotOverflow = 0x80000000u;
 
-template <int MODE>
-__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, int G,
-                                unsigned gm, float mux, float muy, float muz, const EllRec& el,
+template <int MODE, int G>
+__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, unsigned gm, float mux, float muy, float muz, const EllRec& el,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
                                 uint32_t payload, uint4* __restrict__ slot) {
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
@@ -259,8 +266,8 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, i
       vis = true;
     }
   }
-  const int rmin = max(gmin(vis ? ty0 : 0x7fffffff, G), c_fp.row0);
-  const int rmax = min(gmax(vis ? ty1 : -1, G), c_fp.row1 - 1);
+  const int rmin = max(gmin<G>(vis ? ty0 : 0x7fffffff), c_fp.row0);
+  const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
   const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
   const int it_max = __reduce_max_sync(0xffffffffu, nrows);
   const bool lead = (threadIdx.x & (G - 1)) == 0;
@@ -278,7 +285,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, i
         tx1 = q1;
       }
     }
-    const int lo = gmin(tx0, G), hi = gmax(tx1, G);
+    const int lo = gmin<G>(tx0), hi = gmax<G>(tx1);
     const bool any = rowok && hi >= lo;
     const bool narrow = any && hi - lo < 64;
     const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
@@ -287,7 +294,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, i
       const int len = tx1 - tx0 + 1;
       mask = ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - lo);
     }
-    mask = gor64(mask, G);
+    mask = gor64<G>(mask);
     if (narrow) {
       if (MODE == 2 && lead) {
         unsigned long long m = mask;
@@ -343,7 +350,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, i
 // One thread per Gaussian, looping over the K clusters so the SH
 // coefficients are read once and evaluated K times.  Per (k,i), r = k*M + i:
 //   rec0[r] = (A', B', C', log2 o)  conic prescaled by -log2(e)/2, -log2(e)
-//   rec1[r] = (r, g, b, depth)      colour at v'_k, depth d_{i,k}
+//   rec1[r] = (r, g, b, ext)        colour at v'_k; ext = half2 (ex, ey) extents
 //   geom[r] = (a, b, c, det)        exact EWA Sigma2D for the tile test (O6/O7)
 //   dkey[r] = bits(d_{i,k}),  vis[r] = 1 if (i,k) survives culling, else 0
 // ===========================================================================
@@ -420,7 +427,12 @@ __global__ void __launch_bounds__(128) k_preprocess(
           }
           col[ch] = fmaxf(v + 0.5f, 0.0f);
         }
-        rec1[r] = make_float4(col[0], col[1], col[2], p.z);
+        // conservative half extents of the alpha >= 1/255 ellipse (+0.5 px, +0.1%):
+        // the composite uses them to cull (entry, view) pairs that cannot reach a
+        // subpixel (superfluous cluster-union pairs)
+        const float ex = fmaf(sqrtf(tau * a), 1.001f, 0.5f), ey = fmaf(sqrtf(tau * c), 1.001f, 0.5f);
+        const __half2 ext = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
+        rec1[r] = make_float4(col[0], col[1], col[2], *reinterpret_cast<const float*>(&ext));
         dkey[r] = __float_as_uint(p.z);
       }
     }
@@ -443,8 +455,9 @@ __global__ void __launch_bounds__(128) k_preprocess(
 // ===========================================================================
 constexpr int kBinThreads = 256;
 
+template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
-                                                       uint32_t n, int G,
+                                                       uint32_t n,
                                                        const float4* __restrict__ mean4,
                                                        const float4* __restrict__ geom,
                                                        uint32_t* __restrict__ cnt,
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
       q = geom[r];
     }
     const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
-    const uint32_t c = group_union<1>(s_cam, active, k, v, G, gm, m.x, m.y, m.z, el, nullptr,
+    const uint32_t c = group_union<1, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, nullptr,
                                       nullptr, 0, slots + 2ull * r);
     if (active && v == 0) cnt[r] = c;
   }
@@ -521,9 +534,10 @@ __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__
 
 // a6 emit, general path — one G-lane group per listed sorted position e
 // (recomputes the union; n read on the device).
+template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
-    const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr, int G,
+    const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr,
     const float4* __restrict__ mean4, const float4* __restrict__ geom,
     uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
   __shared__ float s_cam[kMaxViews * kCamStride];
@@ -551,7 +565,7 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
       o = offs[e];
     }
     const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
-    group_union<2>(s_cam, active, k, v, G, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r,
+    group_union<2, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r,
                    nullptr);
   }
 }

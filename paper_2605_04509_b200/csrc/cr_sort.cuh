@@ -153,56 +153,106 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_upsweep(
   }
 }
 
-// Stable scatter.  Elements of a block are processed in kSortItems rounds of
-// kSortThreads consecutive elements; within a round, ranks come from
-// __match_any_sync per warp and an exclusive prefix over warps per digit.
+// Stable scatter, three phases per block of kSortTile elements (kSortWarps
+// contiguous warp sub-tiles of kSortItems*32, each walked in order):
+//  1. per round of 32: digit peers by 8-bit ballot multisplit (no MATCH),
+//     the group leader's shared atomicAdd returns the same-digit count of the
+//     warp's earlier rounds -> rank within the warp (kept packed in a register)
+//  2. per digit: exclusive prefix over warps -> block-local offsets; elements
+//     are written digit-sorted into shared memory
+//  3. the block streams shared memory out in order: each digit's run lands
+//     contiguously at its global base (coalesced stores).
 template <bool DIGIT_FROM_VAL, bool MOVE_KEYS>
-__global__ void __launch_bounds__(kSortThreads) k_radix_downsweep(
+__global__ void __launch_bounds__(kSortThreads, 3) k_radix_downsweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
     unsigned long long div, const uint32_t* __restrict__ hist_scanned, int nb) {
-  __shared__ uint32_t s_base[256];            // global base + running count, per digit
-  __shared__ uint32_t s_wc[kSortWarps][256];  // per-warp counts -> per-warp prefixes
+  __shared__ uint32_t s_cnt[kSortWarps][256];  // counts -> block-local warp offsets
+  __shared__ uint32_t s_loff[256];             // block-local digit offsets
+  __shared__ uint32_t s_gbase[256];            // global digit bases of this block
+  __shared__ uint32_t s_k[MOVE_KEYS ? kSortTile : 1];
+  __shared__ uint32_t s_v[kSortTile];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  for (int d = threadIdx.x; d < 256; d += kSortThreads)
-    s_base[d] = hist_scanned[(long long)d * nb + blockIdx.x];
-  for (int q = threadIdx.x; q < kSortWarps * 256; q += kSortThreads) (&s_wc[0][0])[q] = 0;
+  for (int q = threadIdx.x; q < kSortWarps * 256; q += kSortThreads) (&s_cnt[0][0])[q] = 0;
   __syncthreads();
-  const long long base = (long long)blockIdx.x * kSortTile;
+  const long long bbase = (long long)blockIdx.x * kSortTile;
+  const long long wbase = bbase + (long long)w * (kSortItems * 32);
+  uint32_t kr[kSortItems], vr[kSortItems], dl[kSortItems];  // dl = digit | rank << 9
+#pragma unroll
   for (int q = 0; q < kSortItems; ++q) {
-    const long long e = base + q * kSortThreads + threadIdx.x;
-    const bool valid = e < n;
+    const long long e = wbase + q * 32 + lane;
     uint32_t k = 0, v = 0, d = 256;
-    if (valid) {
+    if (e < n) {
       v = vals[e];
       if (MOVE_KEYS || !DIGIT_FROM_VAL) k = keys[e];
       d = DIGIT_FROM_VAL ? ((uint32_t)((unsigned long long)v / div) & 255u) : ((k >> shift) & 255u);
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t rank = __popc(peers & lt);
-    if (valid && rank == 0) s_wc[w][d] = __popc(peers);
-    __syncthreads();
-    // per digit: exclusive prefix over warps, advance the running base
-    for (int dd = threadIdx.x; dd < 256; dd += kSortThreads) {
-      uint32_t acc = s_base[dd];
+    kr[q] = k;
+    vr[q] = v;
+    unsigned peers = __ballot_sync(0xffffffffu, d < 256);
 #pragma unroll
-      for (int ww = 0; ww < kSortWarps; ++ww) {
-        const uint32_t c = s_wc[ww][dd];
-        s_wc[ww][dd] = acc;
-        acc += c;
-      }
-      s_base[dd] = acc;
+    for (int bit = 0; bit < 8; ++bit) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+      peers &= ((d >> bit) & 1u) ? bal : ~bal;
     }
-    __syncthreads();
-    if (valid) {
-      const uint32_t pos = s_wc[w][d] + rank;
-      vals_out[pos] = v;
-      if (MOVE_KEYS) keys_out[pos] = k;
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (d < 256 && lane == leader) old = atomicAdd(&s_cnt[w][d], (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
+    dl[q] = d | ((old + __popc(peers & lt)) << 9);
+  }
+  __syncthreads();
+  // per digit: warp prefix (block-local), block-local digit offsets, global base
+  {
+    const int d = threadIdx.x;  // kSortThreads == 256
+    uint32_t acc = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = s_cnt[ww][d];
+      s_cnt[ww][d] = acc;
+      acc += c;
     }
+    // exclusive scan of the 256 digit totals across the block
+    uint32_t incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t s_ws[kSortWarps];
+    if (lane == 31) s_ws[w] = incl;
     __syncthreads();
-    for (int qq = threadIdx.x; qq < kSortWarps * 256; qq += kSortThreads) (&s_wc[0][0])[qq] = 0;
-    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) wpre += (ww < w) ? s_ws[ww] : 0u;
+    const uint32_t loff = wpre + incl - acc;
+    s_loff[d] = loff;
+    s_gbase[d] = hist_scanned[(long long)d * nb + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) s_cnt[ww][d] += loff;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kSortItems; ++q) {
+    const uint32_t d = dl[q] & 511u;
+    if (d < 256) {
+      const uint32_t p = s_cnt[w][d] + (dl[q] >> 9);
+      s_v[p] = vr[q];
+      if (MOVE_KEYS) s_k[p] = kr[q];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)min((long long)kSortTile, n - bbase);
+  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
+    const uint32_t v = s_v[p];
+    uint32_t k = 0, d;
+    if (MOVE_KEYS) k = s_k[p];
+    if (DIGIT_FROM_VAL) d = (uint32_t)((unsigned long long)v / div) & 255u;
+    else d = (k >> shift) & 255u;
+    const uint32_t gp = s_gbase[d] + ((uint32_t)p - s_loff[d]);
+    vals_out[gp] = v;
+    if (MOVE_KEYS) keys_out[gp] = k;
   }
 }
 
