@@ -101,13 +101,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def band_rows(TY: int, world: int, rank: int):
-    """Contiguous tile-row bands, sizes differing by at most one row."""
-    base, extra = divmod(TY, world)
-    r0 = rank * base + min(rank, extra)
-    return r0, r0 + base + (1 if rank < extra else 0)
-
-
 def compulsory_bytes(cfg, st):
     """SURVEY §8d B_c: scene + records + pairs + view map read + RGB8 write."""
     bg = 44 + 12 * (cfg.sh_degree + 1) ** 2
@@ -225,13 +218,10 @@ def main():
     r.set_display(cfg.W, cfg.H, cfg.N, cfg.lens_pitch, cfg.slant, cfg.center_offset, cfg.view_cone)
     r.set_camera_rig(cams)
     TX, TY = r.TX, r.TY
-    rows = band_rows(TY, world, rank)
-    max_rows = max(band_rows(TY, world, q)[1] - band_rows(TY, world, q)[0] for q in range(world))
-    band_h = max_rows * 16
-    band = torch.zeros((band_h, cfg.W, 3), dtype=torch.uint8, device=dev)
-    full = torch.empty((world * band_h, cfg.W, 3), dtype=torch.uint8, device=dev) if world > 1 else None
-    my_h = min(cfg.H, rows[1] * 16) - rows[0] * 16
-    band_out = band[:my_h]
+    from paper_2605_04509_b200.multigpu import BandGather
+    bgt = BandGather(cfg.H, cfg.W, TY, world, rank, dev)
+    rows = bgt.rows
+    band_out = bgt.out
     remap = not args.no_remap
     kernel = args.kernel if args.kernel is not None else (0 if remap else 1)
     stream = torch.cuda.current_stream(dev)
@@ -239,8 +229,7 @@ def main():
     def step(stats=False, count=False):
         r.render(cfg.cluster_size, remap=remap, kernel=kernel, rows=rows, out=band_out,
                  stats=stats, count_evals=count)
-        if world > 1:
-            dist.all_gather_into_tensor(full, band)
+        bgt.gather()
 
     for _ in range(args.warmup):
         step()
@@ -281,19 +270,11 @@ def main():
     host = torch.empty((cfg.H, cfg.W, 3), dtype=torch.uint8, pin_memory=True)
     rig_bytes = cams.astype(np.float32).nbytes
 
-    def _assemble(f):
-        parts = []
-        for q in range(world):
-            a, b = band_rows(TY, world, q)
-            h = min(cfg.H, b * 16) - a * 16
-            parts.append(f[q * band_h:q * band_h + h])
-        return torch.cat(parts)
-
     def e2e_step():
         r.set_camera_rig(cams)
         if world > 1:
             step()
-            host.copy_(_assemble(full))
+            host.copy_(bgt.frame())
         else:
             r.render(cfg.cluster_size, remap=remap, kernel=kernel, out=host.numpy())
 

@@ -141,15 +141,15 @@ __device__ __forceinline__ bool view_row_cols(const EllRec& e, float mx, float m
   const float dhi = xmin(xsub(xadd(xmul(16.0f, (float)ty), 15.5f), my), e.ey);
   if (dlo > dhi) return false;
   const float dyR = e.dyR, dyL = -e.dyR;
-  const float hlo = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dlo, dlo)))));
-  const float hhi = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dhi, dhi)))));
-  const float bl = xmul(e.b, dlo), bh = xmul(e.b, dhi);
-  const float right = (dlo <= dyR && dyR <= dhi)
-                          ? e.ex
-                          : xmax(xmul(xadd(bl, hlo), e.ic), xmul(xadd(bh, hhi), e.ic));
-  const float left = (dlo <= dyL && dyL <= dhi)
-                         ? -e.ex
-                         : xmin(xmul(xsub(bl, hlo), e.ic), xmul(xsub(bh, hhi), e.ic));
+  const bool rin = dlo <= dyR && dyR <= dhi, lin = dlo <= dyL && dyL <= dhi;
+  float right = e.ex, left = -e.ex;
+  if (!(rin && lin)) {  // the band misses an x-extreme: evaluate the slice ends
+    const float hlo = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dlo, dlo)))));
+    const float hhi = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dhi, dhi)))));
+    const float bl = xmul(e.b, dlo), bh = xmul(e.b, dhi);
+    if (!rin) right = xmax(xmul(xadd(bl, hlo), e.ic), xmul(xadd(bh, hhi), e.ic));
+    if (!lin) left = xmin(xmul(xsub(bl, hlo), e.ic), xmul(xsub(bh, hhi), e.ic));
+  }
   tx0 = clamp_to_int(ceilf(xmul(xsub(xadd(mx, left), 15.5f), 0.0625f)), 0.0f, (float)TX);
   tx1 = clamp_to_int(floorf(xmul(xsub(xadd(mx, right), 0.5f), 0.0625f)), -1.0f, (float)(TX - 1));
   return true;

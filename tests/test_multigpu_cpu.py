@@ -1,0 +1,76 @@
+"""Host logic of the row-band split and the band gather, on CPU with the
+gloo backend at world size 2 (the NCCL path uses the same code on B200)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_04509_b200 import multigpu as mg
+
+
+def test_band_rows_partition():
+    for TY in (1, 9, 135, 270):
+        for world in (1, 2, 3, 4, 8):
+            if world > TY:
+                continue
+            bands = [mg.band_rows(TY, world, r) for r in range(world)]
+            assert bands[0][0] == 0 and bands[-1][1] == TY
+            assert all(bands[q][1] == bands[q + 1][0] for q in range(world - 1))
+            sizes = [b - a for a, b in bands]
+            assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+
+
+def test_pose_split_covers_all():
+    got = sorted(sum((mg.pose_split(256, 8, r) for r in range(8)), []))
+    assert got == list(range(256)) and len(mg.pose_split(256, 8, 3)) == 32
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _frame_ref(H, W):
+    # deterministic stand-in for a rendered frame: value depends on (y, x, u)
+    y, x, u = np.meshgrid(np.arange(H), np.arange(W), np.arange(3), indexing="ij")
+    return ((y * 7 + x * 3 + u * 11) % 251).astype(np.uint8)
+
+
+def _worker(rank, world, port, H, W, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    TY = (H + 15) // 16
+    bg = mg.BandGather(H, W, TY, world, rank, "cpu")
+    ref = _frame_ref(H, W)
+    y0, y1 = mg.band_pixel_rows(H, TY, world, rank)
+    bg.out.copy_(torch.from_numpy(ref[y0:y1]))  # "render" this rank's band
+    bg.gather()
+    full = bg.frame().numpy()
+    q.put((rank, bool(np.array_equal(full, ref)), bg.rows))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("H", [144, 138, 2160])
+def test_gloo_world2_band_gather(H):
+    W, world = 40, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert all(ok for _, ok, _ in res)
+    assert res[0][2][1] == res[1][2][0]  # contiguous bands
