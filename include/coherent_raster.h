@@ -173,7 +173,7 @@ typedef struct {
   int32_t num_clusters;      /* K                                                   */
   int32_t bit_k;             /* Bit_K                                               */
   int32_t launches;          /* kernels launched by this call                       */
-  int32_t reserved;
+  int32_t emit_fallback;     /* records whose tile union did not fit a 32-B slot     */
   float ms_preprocess, ms_bin, ms_sort, ms_composite, ms_total; /* CUDA-event times   */
   int64_t device_bytes;      /* device memory held by the context                   */
   int64_t evals;             /* blend evaluations (only with CR_FLAG_COUNT_EVALS)   */

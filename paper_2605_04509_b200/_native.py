@@ -54,12 +54,12 @@ class Stats(C.Structure):
     _fields_ = [("pairs", C.c_int64), ("visible_ik", C.c_int64), ("culled_near", C.c_int64),
                 ("culled_degenerate", C.c_int64), ("culled_opacity", C.c_int64),
                 ("num_clusters", C.c_int32), ("bit_k", C.c_int32), ("launches", C.c_int32),
-                ("reserved", C.c_int32), ("ms_preprocess", C.c_float), ("ms_bin", C.c_float),
+                ("emit_fallback", C.c_int32), ("ms_preprocess", C.c_float), ("ms_bin", C.c_float),
                 ("ms_sort", C.c_float), ("ms_composite", C.c_float), ("ms_total", C.c_float),
                 ("device_bytes", C.c_int64), ("evals", C.c_int64)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 _lib = None

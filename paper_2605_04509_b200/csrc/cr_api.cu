@@ -45,18 +45,6 @@ struct DevBuf {
 };
 
 struct Scan {  // functors for the generic device scan
-  struct InFlag {
-    const uint32_t* cnt;
-    __device__ uint32_t operator()(long long i) const { return cnt[i] > 0u ? 1u : 0u; }
-  };
-  struct OutCompact {
-    const uint32_t* dkey;
-    uint32_t* ko;
-    uint32_t* vo;
-    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
-      if (v) { ko[ex] = dkey[i]; vo[ex] = (uint32_t)i; }
-    }
-  };
   struct OutIdx {  // compaction: write the index of every flagged element
     uint32_t* o;
     __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
@@ -615,7 +603,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->kb, Rz * 4));
   CR_TRY(ensure(c, c->vb, Rz * 4));
   CR_TRY(ensure(c, c->offs, Rz * 4));
-  CR_TRY(ensure(c, c->slots, Rz * 32));
+  CR_TRY(ensure(c, c->slots, Rz * 64));
   CR_TRY(ensure(c, c->elist, Rz * 4));
   int G = 1;
   while (G < s) G <<= 1;
@@ -801,6 +789,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     st->culled_degenerate = (int64_t)cnts[1];
     st->culled_opacity = (int64_t)cnts[2];
     st->evals = (int64_t)cnts[3];
+    uint32_t nfb = 0;
+    CR_CUDA(c, cudaMemcpy(&nfb, sc + 5, 4, cudaMemcpyDeviceToHost));
+    st->emit_fallback = (int32_t)nfb;
     st->num_clusters = K;
     st->bit_k = bitK;
     st->launches = c->launches;

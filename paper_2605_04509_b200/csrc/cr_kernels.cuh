@@ -238,20 +238,20 @@ __device__ __forceinline__ unsigned long long gor64(unsigned long long v) {
 // band rows, computed by a GROUP of G lanes: lane v of the group owns view
 // j = k*s + v of cluster k (exact per-view mean, Eq.5, and AccuTile rows /
 // per-row columns, O7); per tile row the views' column intervals are merged
-// by shuffles into a 64-bit mask (or, for spans >= 64 tiles, a per-column
-// ballot).  Identical set on every call: same inputs, same exactly-rounded
-// code.  MODE 0 counts; MODE 1 also fills a 32-byte "union slot" (rows of
-// <= 32-tile masks, see k_emit_slots) for the emit pass; MODE 2 writes the
-// tile ids (rows ascending, columns ascending) + payload r.
+// by shuffles into 64-bit masks over 64-column windows.  MODE 0 counts; MODE 2 also writes the tile ids (rows ascending,
+// columns ascending) + payload r.  This is the GENERAL path (any footprint);
+// k_count's fast path handles records of <= kSlotRows rows and < 64 columns
+// and produces the same set (same exactly-rounded per-(view,row) code).
 // Must be called by all 32 lanes of the warp (inactive groups: active=false).
 // ===========================================================================
-constexpr int kSlotRows = 4;
+constexpr int kSlotRows = 6;               // rows of a 64-byte union slot
 constexpr uint32_t kSlotOverflow = 0x80000000u;
 
 template <int MODE, int G>
-__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, unsigned gm, float mux, float muy, float muz, const EllRec& el,
+__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, unsigned gm,
+                                float mux, float muy, float muz, const EllRec& el,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
-                                uint32_t payload, uint4* __restrict__ slot) {
+                                uint32_t payload) {
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int j = k * s + v;
   bool vis = false;
@@ -270,10 +270,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
   const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
   const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
   const int it_max = __reduce_max_sync(0xffffffffu, nrows);
-  const bool lead = (threadIdx.x & (G - 1)) == 0;
   uint32_t n = 0;
-  uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // slot words (MODE 1)
-  bool ovf = nrows > kSlotRows;
   for (int it = 0; it < it_max; ++it) {
     const int ty = rmin + it;
     const bool rowok = it < nrows;
@@ -287,60 +284,36 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
     }
     const int lo = gmin<G>(tx0), hi = gmax<G>(tx1);
     const bool any = rowok && hi >= lo;
-    const bool narrow = any && hi - lo < 64;
     const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
-    unsigned long long mask = 0ull;
-    if (narrow && tx1 >= tx0) {
-      const int len = tx1 - tx0 + 1;
-      mask = ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - lo);
-    }
-    mask = gor64<G>(mask);
-    if (narrow) {
-      if (MODE == 2 && lead) {
-        unsigned long long m = mask;
-        uint32_t q = n;
-        while (m) {
-          const int bit = __ffsll((long long)m) - 1;
-          m &= m - 1;
-          out_t[q] = rowbase + (uint32_t)(lo + bit);
-          out_v[q] = payload;
-          ++q;
+    // merge the views' intervals in 64-column windows (one window unless the
+    // row spans >= 64 tiles), warp-uniform window count
+    const int nwin = any ? ((hi - lo) >> 6) + 1 : 0;
+    const int wmax = __reduce_max_sync(0xffffffffu, nwin);
+    for (int wi = 0; wi < wmax; ++wi) {
+      const int wlo = lo + (wi << 6);
+      unsigned long long mask = 0ull;
+      if (wi < nwin && tx1 >= tx0) {
+        const int a0 = max(tx0, wlo), a1 = min(tx1, wlo + 63);
+        if (a0 <= a1) {
+          const int len = a1 - a0 + 1;
+          mask = ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (a0 - wlo);
         }
       }
-      n += (uint32_t)__popcll(mask);
-    }
-    if (MODE == 1 && rowok && it < kSlotRows) {
-      if (any && !(narrow && hi - lo < 32)) ovf = true;
-      if (narrow && hi - lo < 32) {
-#pragma unroll
-        for (int q = 0; q < kSlotRows; ++q)
-          if (q == it) {
-            sw[1 + (q >> 1)] |= (uint32_t)lo << ((q & 1) * 16);
-            sw[4 + q] = (uint32_t)mask;
+      mask = gor64<G>(mask);
+      if (wi < nwin) {
+        const int pc = __popcll(mask);
+        if (MODE == 2) {  // the group's lanes write ranks v, v+G, ... (ascending tiles)
+          const unsigned lo32 = (unsigned)mask, hi32 = (unsigned)(mask >> 32);
+          const int pl = __popc(lo32);
+          for (int q = (int)(threadIdx.x & (G - 1)); q < pc; q += G) {
+            const int bit = q < pl ? (int)__fns(lo32, 0, q + 1) : 32 + (int)__fns(hi32, 0, q - pl + 1);
+            out_t[n + q] = rowbase + (uint32_t)(wlo + bit);
+            out_v[n + q] = payload;
           }
-      }
-    }
-    // wide rows (>= 64 tiles): per-column ballot, warp-uniform trip count
-    const int span = (any && !narrow) ? hi - lo + 1 : 0;
-    const int smax = __reduce_max_sync(0xffffffffu, span);
-    for (int q = 0; q < smax; ++q) {
-      const int tx = lo + q;
-      const unsigned bal = __ballot_sync(0xffffffffu, q < span && tx0 <= tx && tx <= tx1);
-      if (q < span && (bal & gm) != 0u) {
-        if (MODE == 2 && lead) {
-          out_t[n] = rowbase + (uint32_t)tx;
-          out_v[n] = payload;
         }
-        ++n;
+        n += (uint32_t)pc;
       }
     }
-  }
-  if (MODE == 1 && active && lead) {
-    sw[0] = (uint32_t)(rmin & 0xFFFF) | ((uint32_t)min(nrows, kSlotRows) << 16) |
-            (ovf ? kSlotOverflow : 0u);
-    sw[3] = n;
-    slot[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
-    slot[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
   }
   return n;
 }
@@ -449,11 +422,27 @@ __global__ void __launch_bounds__(128) k_preprocess(
 }
 
 // ===========================================================================
-// a6 count — one G-lane group per visible record (list `recs`, n entries):
-// cnt[r] = |T_{i,k}| in the band.  Grid-stride (persistent) so the camera
-// table is staged in shared memory once per CTA.
+// a6 count — per warp, 32/G records (one G-lane group each, lane = view).
+// Fast path (footprint <= kSlotRows rows, < 64 columns from a conservative
+// reference column lo_ref): the (view, row) items of all the warp's records
+// are redistributed evenly over the 32 lanes (warp prefix + binary search),
+// each item computes its exact AccuTile interval (O7) and ORs it into the
+// record's per-row 64-bit mask in shared memory.  The record's union slot
+// (64 B: header, lo_ref, up to kSlotRows masks) is written for the emit pass.
+// Records outside the fast path take group_union (general, same set) and are
+// flagged in their slot.  Grid-stride, warp-uniform loop; cameras in smem.
 // ===========================================================================
 constexpr int kBinThreads = 256;
+constexpr int kBinWarps = kBinThreads / 32;
+
+struct BinWarpSmem {
+  float mx[32], my[32];
+  int row0[32];                               // first covered row of each view lane
+  int pre[32];                                // inclusive prefix of items per lane
+  float ell[32][8];                           // per group: ex, ey, dyR, tc, ic, b, det
+  int rmin[32], lo_ref[32], flag[32];
+  unsigned long long mask[32][kSlotRows];     // per group, per row
+};
 
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
@@ -463,16 +452,20 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
                                                        uint32_t* __restrict__ cnt,
                                                        uint4* __restrict__ slots) {
   __shared__ float s_cam[kMaxViews * kCamStride];
+  __shared__ BinWarpSmem s_w[kBinWarps];
   stage_cams(s_cam);
   __syncthreads();
+  constexpr int GPW = 32 / G;  // groups (records) per warp
   const unsigned long long M = (unsigned long long)c_fp.M;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1);
+  const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
   const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  const int gpw = 32 / G;  // groups per warp
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * (kBinThreads / 32);
-  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * gpw;
-       wb < n; wb += nwarps * gpw) {  // warp-uniform loop
-    const unsigned long long g = wb + lane / G;
+  const bool lead = v == 0;
+  BinWarpSmem& sw = s_w[threadIdx.x >> 5];
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
+       wb < n; wb += nwarps * GPW) {  // warp-uniform loop
+    const unsigned long long g = wb + gi;
     const bool active = g < n;
     uint32_t r = 0;
     float4 m = make_float4(0.f, 0.f, 0.f, 1.f), q = make_float4(1.f, 0.f, 1.f, 1.f);
@@ -484,17 +477,121 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
       q = geom[r];
     }
     const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
-    const uint32_t c = group_union<1, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, nullptr,
-                                      nullptr, 0, slots + 2ull * r);
-    if (active && v == 0) cnt[r] = c;
+    // ---- per view lane: exact mean (Eq.5) and AccuTile rows (O7)
+    const int j = k * s + v;
+    bool vis = false;
+    float mx = 0.f, my = 0.f;
+    int ty0 = 0x7fffffff, ty1 = -1;
+    if (active && v < s && j < N) {
+      const CamDev cam = load_cam(s_cam, j);
+      const F3 p = cam_point_exact(cam, m.x, m.y, m.z);
+      if (p.z >= c_fp.znear) {
+        mean2d_exact(cam, p, mx, my);
+        view_rows(el, my, TY, ty0, ty1);
+        vis = true;
+      }
+    }
+    const int rmin = max(gmin<G>(vis ? ty0 : 0x7fffffff), c_fp.row0);
+    const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
+    const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
+    // conservative reference column: every exact tx0 of the record is >= lo_ref
+    // unless rounding pushes a slice end past the ellipse extreme (then flag)
+    const float mxmin = __int_as_float(gmin<G>(vis ? __float_as_int(mx) ^ ((__float_as_int(mx) >> 31) & 0x7fffffff) : 0x7f800000));
+    const float mxlo = __int_as_float(__float_as_int(mxmin) ^ ((__float_as_int(mxmin) >> 31) & 0x7fffffff));
+    const int lo_ref = (int)fmaxf(floorf((mxlo - el.ex - 15.5f) * 0.0625f) - 1.0f, -1.0f);
+    const bool fast = nrows > 0 && nrows <= kSlotRows;
+    int ni = 0, first = 0;
+    if (fast && vis) {
+      first = max(ty0, rmin);
+      ni = max(0, min(ty1, rmax) - first + 1);
+    }
+    // warp inclusive prefix of items
+    int pre = ni;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    sw.mx[lane] = mx;
+    sw.my[lane] = my;
+    sw.row0[lane] = first;
+    sw.pre[lane] = pre;
+    if (lead) {
+      sw.rmin[gi] = rmin;
+      sw.lo_ref[gi] = lo_ref;
+      sw.flag[gi] = 0;
+      sw.ell[gi][0] = el.ex; sw.ell[gi][1] = el.ey; sw.ell[gi][2] = el.dyR;
+      sw.ell[gi][3] = el.tc; sw.ell[gi][4] = el.ic; sw.ell[gi][5] = el.b;
+      sw.ell[gi][6] = el.det;
+#pragma unroll
+      for (int t = 0; t < kSlotRows; ++t) sw.mask[gi][t] = 0ull;
+    }
+    __syncwarp();
+    // ---- (view, row) items, evenly over the 32 lanes
+    for (int idx = lane; idx < total; idx += 32) {
+      int lo = 0, hi = 31;  // smallest src with pre[src] > idx
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sw.pre[mid] > idx) hi = mid; else lo = mid + 1;
+      }
+      const int src = lo, gs = src / G;
+      const int prev = (src > 0) ? sw.pre[src - 1] : 0;
+      const int row = sw.row0[src] + (idx - prev);
+      EllRec e;
+      e.ex = sw.ell[gs][0]; e.ey = sw.ell[gs][1]; e.dyR = sw.ell[gs][2]; e.tc = sw.ell[gs][3];
+      e.ic = sw.ell[gs][4]; e.b = sw.ell[gs][5]; e.det = sw.ell[gs][6];
+      int tx0, tx1;
+      if (view_row_cols(e, sw.mx[src], sw.my[src], row, TX, tx0, tx1) && tx0 <= tx1) {
+        const int lr = sw.lo_ref[gs];
+        if (tx0 < lr || tx1 - lr >= 64) {
+          atomicOr(&sw.flag[gs], 1);
+        } else {
+          const int len = tx1 - tx0 + 1;
+          const unsigned long long bits =
+              ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - lr);
+          atomicOr(&sw.mask[gs][row - sw.rmin[gs]], bits);
+        }
+      }
+    }
+    __syncwarp();
+    // ---- finalize fast records; general path for the rest
+    const bool slow = active && nrows > 0 && (!fast || sw.flag[gi] != 0);
+    uint32_t c = 0;
+    if (active && fast && !slow && lead) {
+      uint32_t w2[4] = {0, 0, 0, 0};
+      unsigned long long mk[kSlotRows];
+#pragma unroll
+      for (int t = 0; t < kSlotRows; ++t) {
+        mk[t] = sw.mask[gi][t];
+        c += (uint32_t)__popcll(mk[t]);
+      }
+      w2[0] = (uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16);
+      w2[1] = (uint32_t)lo_ref;
+      w2[2] = c;
+      uint4* sl = slots + 4ull * r;
+      sl[0] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      sl[1] = make_uint4((uint32_t)mk[0], (uint32_t)(mk[0] >> 32), (uint32_t)mk[1], (uint32_t)(mk[1] >> 32));
+      sl[2] = make_uint4((uint32_t)mk[2], (uint32_t)(mk[2] >> 32), (uint32_t)mk[3], (uint32_t)(mk[3] >> 32));
+      sl[3] = make_uint4((uint32_t)mk[4], (uint32_t)(mk[4] >> 32), (uint32_t)mk[5], (uint32_t)(mk[5] >> 32));
+    }
+    if (__any_sync(0xffffffffu, slow)) {
+      const uint32_t cs = group_union<0, G>(s_cam, slow, k, v, gm, m.x, m.y, m.z, el, nullptr,
+                                            nullptr, 0);
+      if (slow) {
+        c = cs;
+        if (lead) slots[4ull * r] = make_uint4(kSlotOverflow, 0u, cs, 0u);
+      }
+    }
+    if (active && lead) cnt[r] = c;
+    __syncwarp();
   }
 }
 
 // ===========================================================================
 // a6 emit, fast path — one thread per depth-sorted record e decodes the union
-// slot written by k_count and writes <tile, r> at offs[e].  Records whose
-// union did not fit a slot (> 4 rows or a row >= 32 tiles) are appended to
-// `elist` for k_emit_groups.
+// slot written by k_count and writes <tile, r> at offs[e].  Records flagged
+// in their slot are appended to `elist` for k_emit_groups.
 // ===========================================================================
 __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__ rec_sorted,
                                                     const uint32_t* __restrict__ offs, uint32_t n,
@@ -506,28 +603,31 @@ __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const uint32_t r = rec_sorted[e];
-  const uint4 h = slots[2ull * r];
+  const uint4* sl = slots + 4ull * r;
+  const uint4 h = sl[0];
   if (h.x & kSlotOverflow) {
     elist[atomicAdd(n_elist, 1u)] = e;
     return;
   }
-  const uint4 mk = slots[2ull * r + 1];
-  const uint32_t row0 = h.x & 0xFFFF, nrows = (h.x >> 16) & 7;
+  const uint32_t row0 = h.x & 0xFFFF, nrows = (h.x >> 16) & 0xFF;
+  const uint32_t lo = h.y;
   const uint32_t TX = (uint32_t)c_fp.TX;
-  const uint32_t lo[4] = {h.y & 0xFFFF, h.y >> 16, h.z & 0xFFFF, h.z >> 16};
-  const uint32_t ms[4] = {mk.x, mk.y, mk.z, mk.w};
   uint32_t o = offs[e];
+  for (uint32_t q = 0; q < nrows; q += 2) {
+    const uint4 mk = sl[1 + (q >> 1)];
+    unsigned long long m2[2] = {(unsigned long long)mk.x | ((unsigned long long)mk.y << 32),
+                                (unsigned long long)mk.z | ((unsigned long long)mk.w << 32)};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if ((uint32_t)q >= nrows) break;
-    uint32_t m = ms[q];
-    const uint32_t base = (row0 + q) * TX + lo[q];
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      out_t[o] = base + bit;
-      out_v[o] = r;
-      ++o;
+    for (int qq = 0; qq < 2; ++qq) {
+      unsigned long long m = (q + qq < nrows) ? m2[qq] : 0ull;
+      const uint32_t base = (row0 + q + qq) * TX + lo;
+      while (m) {
+        const int bit = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        out_t[o] = base + (uint32_t)bit;
+        out_v[o] = r;
+        ++o;
+      }
     }
   }
 }
@@ -547,10 +647,10 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
   const unsigned long long M = (unsigned long long)c_fp.M;
   const int lane = threadIdx.x & 31, v = lane & (G - 1);
   const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  const int gpw = 32 / G;
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * (kBinThreads / 32);
-  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * gpw;
-       wb < n; wb += nwarps * gpw) {
+  constexpr int GPW = 32 / G;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
+       wb < n; wb += nwarps * GPW) {
     const unsigned long long g = wb + lane / G;
     const bool active = g < n;
     uint32_t r = 0, o = 0;
@@ -565,8 +665,7 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
       o = offs[e];
     }
     const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
-    group_union<2, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r,
-                   nullptr);
+    group_union<2, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r);
   }
 }
 
