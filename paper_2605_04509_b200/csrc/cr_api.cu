@@ -557,6 +557,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   FrameParams fp{};
   fp.W = W; fp.H = H; fp.TX = TX; fp.TY = TY; fp.N = N; fp.s = s; fp.K = K; fp.bitK = bitK;
   fp.row0 = row0; fp.row1 = row1; fp.deg = c->deg; fp.remap = o->remap; fp.M = M;
+  fp.divM = make_fastdiv((uint32_t)std::max<long long>(M, 1));
   fp.znear = c->znear;
   for (int u = 0; u < 3; ++u) fp.bg[u] = o->background[u];
   std::vector<int> rep(K);
@@ -593,7 +594,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   const size_t Rz = (size_t)std::max<long long>(R, 1);
   CR_TRY(ensure(c, c->rec0, Rz * 16));
   CR_TRY(ensure(c, c->rec1, Rz * 16));
-  CR_TRY(ensure(c, c->geom, Rz * 16));
+  CR_TRY(ensure(c, c->geom, Rz * 32));
   CR_TRY(ensure(c, c->vis, Rz * 4));
   CR_TRY(ensure(c, c->vlist, Rz * 4));
   CR_TRY(ensure(c, c->cnt, Rz * 4));

@@ -27,12 +27,33 @@ struct CamConstDev {
   float C[3];                        // camera centre -R^T t (O11)
   float pad;
 };
+// n / d for 32-bit n by a runtime divisor (Granlund-Montgomery round-up
+// method): q = umulhi(n, m); (q + ((n - q) >> 1)) >> sh; d == 1 special.
+struct FastDiv {
+  uint32_t d, m, sh;
+};
+__host__ __device__ inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, 0u};
+  if (d <= 1) return f;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+  f.sh = l - 1;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  if (f.d <= 1) return n;
+  const uint32_t q = __umulhi(n, f.m);
+  return (q + ((n - q) >> 1)) >> f.sh;
+}
+
 struct FrameParams {
   int W, H, TX, TY, N, s, K, bitK;
   int row0, row1;  // tile-row band [row0, row1)
   int deg;
   int remap;
   long long M;
+  FastDiv divM;  // record r = k*M + i  ->  k = fdiv(r, divM)
   float znear;
   float bg[3];
 };
@@ -126,6 +147,14 @@ __device__ __forceinline__ EllRec ell_rec(float a, float b, float c, float det, 
   e.dyR = xdiv(xmul(b, e.ex), a);
   e.tc = xmul(tau, c);
   e.ic = xdiv(1.0f, c);
+  return e;
+}
+// the stored form: g0 = (ex, ey, dyR, tc), g1 = (ic, b, det, 0)
+__device__ __forceinline__ EllRec ell_load(const float4& g0, const float4& g1) {
+  EllRec e;
+  e.a = 0.f; e.c = 0.f; e.tau = 0.f;
+  e.ex = g0.x; e.ey = g0.y; e.dyR = g0.z; e.tc = g0.w;
+  e.ic = g1.x; e.b = g1.y; e.det = g1.z;
   return e;
 }
 // row range [ty0, ty1] of one view (mean my)

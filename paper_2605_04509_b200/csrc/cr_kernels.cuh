@@ -324,7 +324,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
 // coefficients are read once and evaluated K times.  Per (k,i), r = k*M + i:
 //   rec0[r] = (A', B', C', log2 o)  conic prescaled by -log2(e)/2, -log2(e)
 //   rec1[r] = (r, g, b, ext)        colour at v'_k; ext = half2 (ex, ey) extents
-//   geom[r] = (a, b, c, det)        exact EWA Sigma2D for the tile test (O6/O7)
+//   geom[2r..2r+1] = exact AccuTile constants (ex, ey, dyR, tc), (1/c, b, det)
 //   dkey[r] = bits(d_{i,k}),  vis[r] = 1 if (i,k) survives culling, else 0
 // ===========================================================================
 constexpr float kLog2e = 1.4426950408889634f;
@@ -365,7 +365,11 @@ __global__ void __launch_bounds__(128) k_preprocess(
         float a, b, c, det;
         if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { vis[r] = 0; ++n_deg; continue; }
         vis[r] = 1;
-        geom[r] = make_float4(a, b, c, det);
+        {  // exact per-record AccuTile constants (O7), used by count and emit
+          const EllRec el = ell_rec(a, b, c, det, tau);
+          geom[2 * r] = make_float4(el.ex, el.ey, el.dyR, el.tc);
+          geom[2 * r + 1] = make_float4(el.ic, el.b, el.det, 0.0f);
+        }
         const float A = c / det, B = -b / det, C = a / det;  // conic (tolerance path)
         rec0[r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
         // SH colour at the representative camera centre (O11)
@@ -452,31 +456,32 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
                                                        uint32_t* __restrict__ cnt,
                                                        uint4* __restrict__ slots) {
   __shared__ float s_cam[kMaxViews * kCamStride];
-  __shared__ BinWarpSmem s_w[kBinWarps];
+  __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
+  __shared__ int s_flag[kBinWarps][32];
   stage_cams(s_cam);
   __syncthreads();
   constexpr int GPW = 32 / G;  // groups (records) per warp
-  const unsigned long long M = (unsigned long long)c_fp.M;
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
   const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   const bool lead = v == 0;
-  BinWarpSmem& sw = s_w[threadIdx.x >> 5];
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
   for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
        wb < n; wb += nwarps * GPW) {  // warp-uniform loop
     const unsigned long long g = wb + gi;
     const bool active = g < n;
     uint32_t r = 0;
-    float4 m = make_float4(0.f, 0.f, 0.f, 1.f), q = make_float4(1.f, 0.f, 1.f, 1.f);
+    float4 m = make_float4(0.f, 0.f, 0.f, 1.f);
+    float4 q0 = make_float4(1.f, 1.f, 0.f, 1.f), q1 = make_float4(1.f, 0.f, 1.f, 0.f);
     int k = 0;
     if (active) {
       r = recs[g];
-      k = (int)(r / M);
-      m = mean4[(long long)r - (long long)k * (long long)M];
-      q = geom[r];
+      k = (int)fdiv(r, c_fp.divM);
+      m = mean4[(long long)r - (long long)k * c_fp.M];
+      q0 = geom[2ull * r];
+      q1 = geom[2ull * r + 1];
     }
-    const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
+    const EllRec el = ell_load(q0, q1);
     // ---- per view lane: exact mean (Eq.5) and AccuTile rows (O7)
     const int j = k * s + v;
     bool vis = false;
@@ -495,9 +500,10 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
     const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
     const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
     // conservative reference column: every exact tx0 of the record is >= lo_ref
-    // unless rounding pushes a slice end past the ellipse extreme (then flag)
-    const float mxmin = __int_as_float(gmin<G>(vis ? __float_as_int(mx) ^ ((__float_as_int(mx) >> 31) & 0x7fffffff) : 0x7f800000));
-    const float mxlo = __int_as_float(__float_as_int(mxmin) ^ ((__float_as_int(mxmin) >> 31) & 0x7fffffff));
+    // unless rounding pushes a slice end past the ellipse extreme (then flagged)
+    const int xk = __float_as_int(mx);
+    const int kmin = gmin<G>(vis ? (xk ^ ((xk >> 31) & 0x7fffffff)) : 0x7f800000);
+    const float mxlo = __int_as_float(kmin ^ ((kmin >> 31) & 0x7fffffff));
     const int lo_ref = (int)fmaxf(floorf((mxlo - el.ex - 15.5f) * 0.0625f) - 1.0f, -1.0f);
     const bool fast = nrows > 0 && nrows <= kSlotRows;
     int ni = 0, first = 0;
@@ -505,72 +511,75 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
       first = max(ty0, rmin);
       ni = max(0, min(ty1, rmax) - first + 1);
     }
-    // warp inclusive prefix of items
-    int pre = ni;
+    if (lead) {
+      s_flag[w][gi] = 0;
+#pragma unroll
+      for (int t = 0; t < kSlotRows; ++t) s_mask[w][gi][t] = 0ull;
+    }
+    int pre = ni;  // warp inclusive prefix of (view,row) items
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, pre, o);
       if (lane >= o) pre += y;
     }
     const int total = __shfl_sync(0xffffffffu, pre, 31);
-    sw.mx[lane] = mx;
-    sw.my[lane] = my;
-    sw.row0[lane] = first;
-    sw.pre[lane] = pre;
-    if (lead) {
-      sw.rmin[gi] = rmin;
-      sw.lo_ref[gi] = lo_ref;
-      sw.flag[gi] = 0;
-      sw.ell[gi][0] = el.ex; sw.ell[gi][1] = el.ey; sw.ell[gi][2] = el.dyR;
-      sw.ell[gi][3] = el.tc; sw.ell[gi][4] = el.ic; sw.ell[gi][5] = el.b;
-      sw.ell[gi][6] = el.det;
-#pragma unroll
-      for (int t = 0; t < kSlotRows; ++t) sw.mask[gi][t] = 0ull;
-    }
+    const int seg0 = pre - ni;  // this lane's first item
     __syncwarp();
-    // ---- (view, row) items, evenly over the 32 lanes
-    for (int idx = lane; idx < total; idx += 32) {
-      int lo = 0, hi = 31;  // smallest src with pre[src] > idx
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sw.pre[mid] > idx) hi = mid; else lo = mid + 1;
-      }
-      const int src = lo, gs = src / G;
-      const int prev = (src > 0) ? sw.pre[src - 1] : 0;
-      const int row = sw.row0[src] + (idx - prev);
+    // ---- (view, row) items, 32 per window: lane i takes item base+i
+    for (int base = 0; base < total; base += 32) {
+      const bool inter = ni > 0 && pre > base && seg0 < base + 32;
+      const unsigned ib = __ballot_sync(0xffffffffu, inter);
+      const unsigned marks = __reduce_or_sync(0xffffffffu, inter ? (1u << (max(seg0, base) - base)) : 0u);
+      const int idx = base + lane;
+      const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+      const int kk = __popc(marks & upto);
+      const int src = (idx < total && kk > 0) ? (int)__fns(ib, 0, kk) : 0;
+      const float smx = __shfl_sync(0xffffffffu, mx, src);
+      const float smy = __shfl_sync(0xffffffffu, my, src);
+      const int sfirst = __shfl_sync(0xffffffffu, first, src);
+      const int sseg0 = __shfl_sync(0xffffffffu, seg0, src);
+      const int srmin = __shfl_sync(0xffffffffu, rmin, src);
+      const int slo = __shfl_sync(0xffffffffu, lo_ref, src);
       EllRec e;
-      e.ex = sw.ell[gs][0]; e.ey = sw.ell[gs][1]; e.dyR = sw.ell[gs][2]; e.tc = sw.ell[gs][3];
-      e.ic = sw.ell[gs][4]; e.b = sw.ell[gs][5]; e.det = sw.ell[gs][6];
-      int tx0, tx1;
-      if (view_row_cols(e, sw.mx[src], sw.my[src], row, TX, tx0, tx1) && tx0 <= tx1) {
-        const int lr = sw.lo_ref[gs];
-        if (tx0 < lr || tx1 - lr >= 64) {
-          atomicOr(&sw.flag[gs], 1);
-        } else {
-          const int len = tx1 - tx0 + 1;
-          const unsigned long long bits =
-              ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - lr);
-          atomicOr(&sw.mask[gs][row - sw.rmin[gs]], bits);
+      e.ex = __shfl_sync(0xffffffffu, el.ex, src);
+      e.ey = __shfl_sync(0xffffffffu, el.ey, src);
+      e.dyR = __shfl_sync(0xffffffffu, el.dyR, src);
+      e.tc = __shfl_sync(0xffffffffu, el.tc, src);
+      e.ic = __shfl_sync(0xffffffffu, el.ic, src);
+      e.b = __shfl_sync(0xffffffffu, el.b, src);
+      e.det = __shfl_sync(0xffffffffu, el.det, src);
+      if (idx < total) {
+        const int gs = src / G;
+        const int row = sfirst + (idx - sseg0);
+        int tx0, tx1;
+        if (view_row_cols(e, smx, smy, row, TX, tx0, tx1) && tx0 <= tx1) {
+          if (tx0 < slo || tx1 - slo >= 64) {
+            atomicOr(&s_flag[w][gs], 1);
+          } else {
+            const int len = tx1 - tx0 + 1;
+            const unsigned long long bits =
+                ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - slo);
+            // two native 32-bit shared ORs (a 64-bit OR would be a CAS loop)
+            unsigned* mw = reinterpret_cast<unsigned*>(&s_mask[w][gs][row - srmin]);
+            if ((unsigned)bits) atomicOr(mw, (unsigned)bits);
+            if ((unsigned)(bits >> 32)) atomicOr(mw + 1, (unsigned)(bits >> 32));
+          }
         }
       }
     }
     __syncwarp();
     // ---- finalize fast records; general path for the rest
-    const bool slow = active && nrows > 0 && (!fast || sw.flag[gi] != 0);
+    const bool slow = active && nrows > 0 && (!fast || s_flag[w][gi] != 0);
     uint32_t c = 0;
     if (active && fast && !slow && lead) {
-      uint32_t w2[4] = {0, 0, 0, 0};
       unsigned long long mk[kSlotRows];
 #pragma unroll
       for (int t = 0; t < kSlotRows; ++t) {
-        mk[t] = sw.mask[gi][t];
+        mk[t] = s_mask[w][gi][t];
         c += (uint32_t)__popcll(mk[t]);
       }
-      w2[0] = (uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16);
-      w2[1] = (uint32_t)lo_ref;
-      w2[2] = c;
       uint4* sl = slots + 4ull * r;
-      sl[0] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      sl[0] = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
       sl[1] = make_uint4((uint32_t)mk[0], (uint32_t)(mk[0] >> 32), (uint32_t)mk[1], (uint32_t)(mk[1] >> 32));
       sl[2] = make_uint4((uint32_t)mk[2], (uint32_t)(mk[2] >> 32), (uint32_t)mk[3], (uint32_t)(mk[3] >> 32));
       sl[3] = make_uint4((uint32_t)mk[4], (uint32_t)(mk[4] >> 32), (uint32_t)mk[5], (uint32_t)(mk[5] >> 32));
@@ -644,7 +653,6 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
-  const unsigned long long M = (unsigned long long)c_fp.M;
   const int lane = threadIdx.x & 31, v = lane & (G - 1);
   const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   constexpr int GPW = 32 / G;
@@ -654,17 +662,19 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
     const unsigned long long g = wb + lane / G;
     const bool active = g < n;
     uint32_t r = 0, o = 0;
-    float4 m = make_float4(0.f, 0.f, 0.f, 1.f), q = make_float4(1.f, 0.f, 1.f, 1.f);
+    float4 m = make_float4(0.f, 0.f, 0.f, 1.f);
+    float4 q0 = make_float4(1.f, 1.f, 0.f, 1.f), q1 = make_float4(1.f, 0.f, 1.f, 0.f);
     int k = 0;
     if (active) {
       const uint32_t e = elist ? elist[g] : (uint32_t)g;
       r = rec_sorted[e];
-      k = (int)(r / M);
-      m = mean4[(long long)r - (long long)k * (long long)M];
-      q = geom[r];
+      k = (int)fdiv(r, c_fp.divM);
+      m = mean4[(long long)r - (long long)k * c_fp.M];
+      q0 = geom[2ull * r];
+      q1 = geom[2ull * r + 1];
       o = offs[e];
     }
-    const EllRec el = ell_rec(q.x, q.y, q.z, q.w, m.w);
+    const EllRec el = ell_load(q0, q1);
     group_union<2, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r);
   }
 }
@@ -676,13 +686,12 @@ __global__ void k_ranges(const uint32_t* __restrict__ tkey, const uint32_t* __re
                          uint32_t P, uint32_t* __restrict__ S, uint32_t* __restrict__ E) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= P) return;
-  const unsigned long long M = (unsigned long long)c_fp.M;
   const int K = c_fp.K;
   const uint32_t t = tkey[e];
-  const uint32_t k = (uint32_t)(val[e] / M);
+  const uint32_t k = fdiv(val[e], c_fp.divM);
   const uint32_t slot = t * K + k;
-  if (e == 0 || tkey[e - 1] != t || (uint32_t)(val[e - 1] / M) != k) S[slot] = e;
-  if (e == P - 1 || tkey[e + 1] != t || (uint32_t)(val[e + 1] / M) != k) E[slot] = e + 1;
+  if (e == 0 || tkey[e - 1] != t || fdiv(val[e - 1], c_fp.divM) != k) S[slot] = e;
+  if (e == P - 1 || tkey[e + 1] != t || fdiv(val[e + 1], c_fp.divM) != k) E[slot] = e + 1;
 }
 
 // Introspection: 64-bit keys of Eq.11 and payload i.
@@ -693,7 +702,7 @@ __global__ void k_make_keys(const uint32_t* __restrict__ tkey, const uint32_t* _
   if (e >= P) return;
   const unsigned long long M = (unsigned long long)c_fp.M;
   const uint32_t r = val[e];
-  const unsigned long long k = r / M;
+  const unsigned long long k = fdiv(r, c_fp.divM);
   keys[e] = ((unsigned long long)tkey[e] << (32 + c_fp.bitK)) | (k << 32) |
             (unsigned long long)dkey[r];
   pay[e] = (uint32_t)(r - k * M);

@@ -120,13 +120,13 @@ constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements per block
 constexpr int kSortWarps = kSortThreads / 32;
 
-// DIGIT_FROM_VAL: digit = val / div (cluster id of record index r = k*M+i);
+// DIGIT_FROM_VAL: digit = val / M (cluster id of record index r = k*M+i, via c_fp.divM);
 // otherwise digit = (key >> shift) & 255.
 template <bool DIGIT_FROM_VAL>
 __device__ __forceinline__ uint32_t sort_digit(const uint32_t* __restrict__ keys,
                                                const uint32_t* __restrict__ vals, long long e,
                                                int shift, unsigned long long div) {
-  if (DIGIT_FROM_VAL) return (uint32_t)((unsigned long long)vals[e] / div) & 255u;
+  if (DIGIT_FROM_VAL) return fdiv(vals[e], c_fp.divM) & 255u;
   return (keys[e] >> shift) & 255u;
 }
 
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_downsweep(
     if (e < n) {
       v = vals[e];
       if (MOVE_KEYS || !DIGIT_FROM_VAL) k = keys[e];
-      d = DIGIT_FROM_VAL ? ((uint32_t)((unsigned long long)v / div) & 255u) : ((k >> shift) & 255u);
+      d = DIGIT_FROM_VAL ? (fdiv(v, c_fp.divM) & 255u) : ((k >> shift) & 255u);
     }
     kr[q] = k;
     vr[q] = v;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_downsweep(
     const uint32_t v = s_v[p];
     uint32_t k = 0, d;
     if (MOVE_KEYS) k = s_k[p];
-    if (DIGIT_FROM_VAL) d = (uint32_t)((unsigned long long)v / div) & 255u;
+    if (DIGIT_FROM_VAL) d = fdiv(v, c_fp.divM) & 255u;
     else d = (k >> shift) & 255u;
     const uint32_t gp = s_gbase[d] + ((uint32_t)p - s_loff[d]);
     vals_out[gp] = v;
