@@ -747,7 +747,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   const bool count = (o->flags & CR_FLAG_COUNT_EVALS) != 0;
   unsigned long long* evals = counters + 3;
 #define CR_STAGED(F, CNT)                                                                     \
-  k_composite_staged<F, CNT><<<ntile, kCompWarps * 32, 0, str>>>(                             \
+  k_composite_staged<F, CNT, kCompWarps, 0><<<ntile, kCompWarps * 32, 0, str>>>(             \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
       P_<float4>(c->rec0), P_<float4>(c->rec1), m4, dst, evals)

@@ -94,9 +94,10 @@ __global__ void k_remap_build(const uint8_t* __restrict__ V, uint16_t* __restric
   for (int r = nvalid + lane; r < kTileSub; r += 32) out[r] = 0xFFFF;
 }
 
-// Composite work items: per tile, "cluster-aligned warp chunks" of <= 32
+// Composite work items: per tile, "cluster-aligned chunks" of <= kChunkMax
 // consecutive Psi ranks that share one cluster k (DESIGN.md §5 composite).
 // Packed as start | (len-1) << 10 | k << 16.  One thread per tile.
+constexpr int kChunkMax = 32;
 __global__ void k_chunks_build(const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,
                                uint32_t* __restrict__ chunks, uint32_t* __restrict__ nchunks,
                                int stride, int W, int TX, int TY, int s) {
@@ -112,7 +113,7 @@ __global__ void k_chunks_build(const uint8_t* __restrict__ V, const uint16_t* __
     const int ly = l / 48, rem = l % 48, lx = rem / 3, u = rem % 3;
     const int j = V[((long long)(ty * 16 + ly) * W + tx * 16 + lx) * 3 + u];
     const int k = j / s;
-    if (k != seg_k || r - seg_start == 32) {
+    if (k != seg_k || r - seg_start == kChunkMax) {
       if (seg_k >= 0) out[n++] = (uint32_t)seg_start | ((uint32_t)(r - seg_start - 1) << 10) |
                                  ((uint32_t)seg_k << 16);
       seg_k = k;
