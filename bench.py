@@ -184,7 +184,8 @@ def main():
     ap.add_argument("--no-remap", action="store_true")
     ap.add_argument("--kernel", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=4, help="oracle sample: tile rows")
+    ap.add_argument("--ref-rows", type=int, default=None,
+                    help="oracle sample: tile rows (default 12 for cpu_baseline, 4 per --impl reference step)")
     ap.add_argument("--ablation", action="store_true", help="also time reuse/remap variants (stderr)")
     args = ap.parse_args()
 
@@ -195,8 +196,12 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
+        if args.ref_rows is None:
+            args.ref_rows = 4
         run_reference(args, cfg)
         return
+    if args.ref_rows is None:
+        args.ref_rows = 12
 
     import torch
     import torch.distributed as dist
@@ -332,7 +337,7 @@ def main():
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"config {cfg.name}: {cfg.M} Gaussians SH{cfg.sh_degree} "
                                f"(scene_gen v1), {cfg.N}-view lenticular {cfg.W}x{cfg.H}",
