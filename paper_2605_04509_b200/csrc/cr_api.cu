@@ -104,7 +104,7 @@ struct cr_ctx {
   std::vector<CamConstDev> ccon;
   float znear = 0.01f;
   // frame buffers
-  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, vlist, slots, elist;
+  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, vlist, slots, elist, biglist;
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
   DevBuf bsum, hist, scalars, S, E, stage_out;
@@ -347,7 +347,7 @@ void cr_destroy(cr_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
-                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
+                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->tmp};
   for (DevBuf* b : all) release(*b);
@@ -409,7 +409,7 @@ cr_status cr_upload_gaussians(cr_ctx* c, int64_t M, int deg, const float* means,
   CR_TRY(ensure(c, c->mean4, 16 * (size_t)M));
   CR_TRY(ensure(c, c->cov8, 32 * (size_t)M));
   CR_TRY(ensure(c, c->shsoa, 4 * (size_t)M * nc3));
-  int* flag = P_<int>(c->scalars) + 6;
+  int* flag = P_<int>(c->scalars) + 7;
   CR_CUDA(c, cudaMemsetAsync(flag, 0, 4, c->stream));
   k_upload<<<grid_for(M, 256), 256, 0, c->stream>>>(M, nc3, d_means, d_quats, d_scales, d_op,
                                                      d_tau, d_sh, P_<float4>(c->mean4),
@@ -606,6 +606,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->offs, Rz * 4));
   CR_TRY(ensure(c, c->slots, Rz * 64));
   CR_TRY(ensure(c, c->elist, Rz * 4));
+  CR_TRY(ensure(c, c->biglist, Rz * 4));
   int G = 1;
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
@@ -632,10 +633,15 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     CR_TRY(read_u32(c, sc + 4, &nvis0));
     CR_CUDA(c, cudaMemsetAsync(c->cnt.p, 0, (size_t)R * 4, str));
     if (nvis0 > 0) {
-#define CR_COUNT(GG)                                                                        \
-  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0,             \
-                                                 P_<float4>(c->mean4), P_<float4>(c->geom), \
-                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots))
+#define CR_COUNT(GG)                                                                          \
+  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0,               \
+                                                 P_<float4>(c->mean4), P_<float4>(c->geom),   \
+                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots),   \
+                                                 P_<uint32_t>(c->biglist), sc + 6);           \
+  CR_LAUNCHED(c);                                                                             \
+  k_count_big<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->biglist), sc + 6,        \
+                                                     P_<float4>(c->mean4), P_<float4>(c->geom), \
+                                                     P_<uint32_t>(c->cnt))
       switch (G) {
         case 1: CR_COUNT(1); break;
         case 2: CR_COUNT(2); break;
@@ -699,7 +705,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
                                                        P_<uint32_t>(c->elist), n_el);
     CR_LAUNCHED(c);
 #define CR_EMITG(GG)                                                                        \
-  k_emit_groups<GG><<<bin_grid, kBinThreads, 0, str>>>(                                     \
+  k_emit_big<GG><<<bin_grid, kBinThreads, 0, str>>>(                                        \
       rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->elist), n_el, P_<float4>(c->mean4), \
       P_<float4>(c->geom), tA, pA)
     switch (G) {

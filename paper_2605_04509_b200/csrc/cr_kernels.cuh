@@ -249,10 +249,14 @@ constexpr int kSlotRows = 6;               // rows of a 64-byte union slot
 constexpr uint32_t kSlotOverflow = 0x80000000u;
 
 template <int MODE, int G>
-__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, unsigned gm,
-                                float mux, float muy, float muz, const EllRec& el,
+__device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, float mux,
+                                float muy, float muz, const EllRec& el, int it0, int istep,
+                                uint32_t* __restrict__ row_cnt, const uint32_t* __restrict__ row_off,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
                                 uint32_t payload) {
+  // MODE 0: count the group's rows; MODE 3: also store per-row counts in
+  // row_cnt[it]; MODE 2: write the tiles of row it at row_off[it] + rank.
+  // The group handles union rows it = it0, it0 + istep, ...
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int j = k * s + v;
   bool vis = false;
@@ -270,11 +274,14 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
   const int rmin = max(gmin<G>(vis ? ty0 : 0x7fffffff), c_fp.row0);
   const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
   const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
-  const int it_max = __reduce_max_sync(0xffffffffu, nrows);
+  const int mine = nrows > it0 ? (nrows - it0 + istep - 1) / istep : 0;
+  const int it_max = __reduce_max_sync(0xffffffffu, mine);
+  const bool lead = (threadIdx.x & (G - 1)) == 0;
   uint32_t n = 0;
-  for (int it = 0; it < it_max; ++it) {
+  for (int ii = 0; ii < it_max; ++ii) {
+    const int it = it0 + ii * istep;
     const int ty = rmin + it;
-    const bool rowok = it < nrows;
+    const bool rowok = ii < mine;
     int tx0 = 0x7fffffff, tx1 = -1;
     if (rowok && vis && ty >= ty0 && ty <= ty1) {
       int q0, q1;
@@ -286,6 +293,8 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
     const int lo = gmin<G>(tx0), hi = gmax<G>(tx1);
     const bool any = rowok && hi >= lo;
     const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
+    uint32_t rowpos = (MODE == 2 && rowok) ? row_off[it] : 0u;
+    uint32_t rown = 0;
     // merge the views' intervals in 64-column windows (one window unless the
     // row spans >= 64 tiles), warp-uniform window count
     const int nwin = any ? ((hi - lo) >> 6) + 1 : 0;
@@ -308,13 +317,16 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, u
           const int pl = __popc(lo32);
           for (int q = (int)(threadIdx.x & (G - 1)); q < pc; q += G) {
             const int bit = q < pl ? (int)__fns(lo32, 0, q + 1) : 32 + (int)__fns(hi32, 0, q - pl + 1);
-            out_t[n + q] = rowbase + (uint32_t)(wlo + bit);
-            out_v[n + q] = payload;
+            out_t[rowpos + q] = rowbase + (uint32_t)(wlo + bit);
+            out_v[rowpos + q] = payload;
           }
+          rowpos += (uint32_t)pc;
         }
-        n += (uint32_t)pc;
+        rown += (uint32_t)pc;
       }
     }
+    if (MODE == 3 && lead && rowok) row_cnt[it] = rown;
+    n += rown;
   }
   return n;
 }
@@ -455,7 +467,9 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
                                                        const float4* __restrict__ mean4,
                                                        const float4* __restrict__ geom,
                                                        uint32_t* __restrict__ cnt,
-                                                       uint4* __restrict__ slots) {
+                                                       uint4* __restrict__ slots,
+                                                       uint32_t* __restrict__ big,
+                                                       uint32_t* __restrict__ n_big) {
   __shared__ float s_cam[kMaxViews * kCamStride];
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
@@ -464,7 +478,6 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
   constexpr int GPW = 32 / G;  // groups (records) per warp
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
-  const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   const bool lead = v == 0;
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
   for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
@@ -585,13 +598,9 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
       sl[2] = make_uint4((uint32_t)mk[2], (uint32_t)(mk[2] >> 32), (uint32_t)mk[3], (uint32_t)(mk[3] >> 32));
       sl[3] = make_uint4((uint32_t)mk[4], (uint32_t)(mk[4] >> 32), (uint32_t)mk[5], (uint32_t)(mk[5] >> 32));
     }
-    if (__any_sync(0xffffffffu, slow)) {
-      const uint32_t cs = group_union<0, G>(s_cam, slow, k, v, gm, m.x, m.y, m.z, el, nullptr,
-                                            nullptr, 0);
-      if (slow) {
-        c = cs;
-        if (lead) slots[4ull * r] = make_uint4(kSlotOverflow, 0u, cs, 0u);
-      }
+    if (slow && lead) {  // footprint beyond the fast path: k_count_big
+      slots[4ull * r] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
+      big[atomicAdd(n_big, 1u)] = r;
     }
     if (active && lead) cnt[r] = c;
     __syncwarp();
@@ -642,41 +651,80 @@ __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__
   }
 }
 
-// a6 emit, general path — one G-lane group per listed sorted position e
-// (recomputes the union; n read on the device).
+// ===========================================================================
+// Records whose union exceeds the fast path (> kSlotRows rows or >= 64
+// columns): one WARP per record; its 32/G groups each compute all views and
+// take interleaved union rows (it = g, g + 32/G, ...).
+// ===========================================================================
 template <int G>
-__global__ void __launch_bounds__(kBinThreads) k_emit_groups(
+__global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __restrict__ big,
+                                                           const uint32_t* __restrict__ n_ptr,
+                                                           const float4* __restrict__ mean4,
+                                                           const float4* __restrict__ geom,
+                                                           uint32_t* __restrict__ cnt) {
+  __shared__ float s_cam[kMaxViews * kCamStride];
+  stage_cams(s_cam);
+  __syncthreads();
+  const uint32_t n = *n_ptr;
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
+  const uint32_t nwarps = gridDim.x * kBinWarps;
+  for (uint32_t g = (blockIdx.x * kBinThreads + threadIdx.x) / 32; g < n; g += nwarps) {
+    const uint32_t r = big[g];
+    const int k = (int)fdiv(r, c_fp.divM);
+    const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
+    const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
+    const uint32_t c = group_union<0, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr,
+                                         nullptr, nullptr, nullptr, 0);
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, v == 0 ? c : 0u);
+    if (lane == 0) cnt[r] = tot;
+  }
+}
+
+constexpr int kMaxRows = 288;  // >= TY for 8K (270 tile rows)
+template <int G>
+__global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
     const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr,
     const float4* __restrict__ mean4, const float4* __restrict__ geom,
     uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
   __shared__ float s_cam[kMaxViews * kCamStride];
+  __shared__ uint32_t s_rows[kBinWarps][kMaxRows];
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1);
-  const unsigned gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   constexpr int GPW = 32 / G;
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
-  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
-       wb < n; wb += nwarps * GPW) {
-    const unsigned long long g = wb + lane / G;
-    const bool active = g < n;
-    uint32_t r = 0, o = 0;
-    float4 m = make_float4(0.f, 0.f, 0.f, 1.f);
-    float4 q0 = make_float4(1.f, 1.f, 0.f, 1.f), q1 = make_float4(1.f, 0.f, 1.f, 0.f);
-    int k = 0;
-    if (active) {
-      const uint32_t e = elist ? elist[g] : (uint32_t)g;
-      r = rec_sorted[e];
-      k = (int)fdiv(r, c_fp.divM);
-      m = mean4[(long long)r - (long long)k * c_fp.M];
-      q0 = geom[2ull * r];
-      q1 = geom[2ull * r + 1];
-      o = offs[e];
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
+  uint32_t* rows = s_rows[threadIdx.x >> 5];
+  const uint32_t nwarps = gridDim.x * kBinWarps;
+  for (uint32_t g = (blockIdx.x * kBinThreads + threadIdx.x) / 32; g < n; g += nwarps) {
+    const uint32_t e = elist[g];
+    const uint32_t r = rec_sorted[e];
+    const int k = (int)fdiv(r, c_fp.divM);
+    const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
+    const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
+    for (int q = lane; q < kMaxRows; q += 32) rows[q] = 0;
+    __syncwarp();
+    group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
+                      nullptr, 0);
+    __syncwarp();
+    // exclusive scan of the per-row counts -> row offsets (in place)
+    uint32_t carry = offs[e];
+    for (int b0 = 0; b0 < kMaxRows; b0 += 32) {
+      const uint32_t x = rows[b0 + lane];
+      uint32_t incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      rows[b0 + lane] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    const EllRec el = ell_load(q0, q1);
-    group_union<2, G>(s_cam, active, k, v, gm, m.x, m.y, m.z, el, out_t + o, out_v + o, r);
+    __syncwarp();
+    group_union<2, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, rows, out_t, out_v,
+                      r);
+    __syncwarp();
   }
 }
 
@@ -685,14 +733,20 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_groups(
 // ===========================================================================
 __global__ void k_ranges(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ val,
                          uint32_t P, uint32_t* __restrict__ S, uint32_t* __restrict__ E) {
+  // one load of (t, k) per element; neighbours via shuffles (lanes 0/31 load
+  // their outer neighbour once)
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= P) return;
+  const int lane = threadIdx.x & 31;
   const int K = c_fp.K;
-  const uint32_t t = tkey[e];
-  const uint32_t k = fdiv(val[e], c_fp.divM);
-  const uint32_t slot = t * K + k;
-  if (e == 0 || tkey[e - 1] != t || fdiv(val[e - 1], c_fp.divM) != k) S[slot] = e;
-  if (e == P - 1 || tkey[e + 1] != t || fdiv(val[e + 1], c_fp.divM) != k) E[slot] = e + 1;
+  uint32_t key = 0xFFFFFFFFu;
+  if (e < P) key = tkey[e] * (uint32_t)K + fdiv(val[e], c_fp.divM);  // slot t*K + k
+  uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  uint32_t next = __shfl_down_sync(0xffffffffu, key, 1);
+  if (lane == 0) prev = (e > 0 && e < P) ? tkey[e - 1] * (uint32_t)K + fdiv(val[e - 1], c_fp.divM) : 0xFFFFFFFEu;
+  if (lane == 31) next = (e + 1 < P) ? tkey[e + 1] * (uint32_t)K + fdiv(val[e + 1], c_fp.divM) : 0xFFFFFFFEu;
+  if (e >= P) return;
+  if (e == 0 || prev != key) S[key] = e;
+  if (e == P - 1 || next != key) E[key] = e + 1;
 }
 
 // Introspection: 64-bit keys of Eq.11 and payload i.

@@ -22,6 +22,7 @@ for r in rows[2:]:
     n = n.split('<')[0] + ('<' + r[ki].split('<')[1].split('>')[0] + '>' if '<' in r[ki].split('(')[0] else '')
     a = agg.setdefault(n, [0, 0.0, 0.0, 0.0, 0.0, 0.0])
     a[0] += 1; a[1] += val(r, du); a[2] += val(r, dr) + val(r, dw); a[3] += val(r, ipc); a[4] += val(r, occ)
+lt = col('lts__t_bytes.sum')
 print(f"{'kernel':40s} {'n':>3s} {'time ms':>9s} {'DRAM GB':>8s} {'GB/s':>8s} {'IPC':>5s} {'occ%':>5s}")
 for n, (c, t, b, i, o, _) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"{n[:40]:40s} {c:3d} {t*1e3:9.3f} {b/1e9:8.3f} {b/t/1e9 if t else 0:8.0f} {i/c:5.2f} {o/c:5.1f}")
