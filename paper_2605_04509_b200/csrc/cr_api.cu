@@ -592,8 +592,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 
   // ---- a4 preprocess + SH, a6 count, compaction of records with >= 1 tile
   const size_t Rz = (size_t)std::max<long long>(R, 1);
-  CR_TRY(ensure(c, c->rec0, Rz * 16));
-  CR_TRY(ensure(c, c->rec1, Rz * 16));
+  CR_TRY(ensure(c, c->rec0, Rz * 32));  // AoS 32-byte records (rec1 unused)
   CR_TRY(ensure(c, c->geom, Rz * 32));
   CR_TRY(ensure(c, c->vis, Rz * 4));
   CR_TRY(ensure(c, c->vlist, Rz * 4));
@@ -616,7 +615,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 #define CR_PRE(D)                                                                               \
   k_preprocess<D><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
                                       P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
-                                      P_<float4>(c->rec1), P_<float4>(c->geom),                 \
+                                      P_<float4>(c->rec0) + 1, P_<float4>(c->geom),                 \
                                       P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters)
     switch (c->deg) {
       case 0: CR_PRE(0); break;
@@ -756,11 +755,11 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   k_composite_staged<F, CNT, kCompWarps, 0><<<ntile, kCompWarps * 32, 0, str>>>(             \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
-      P_<float4>(c->rec0), P_<float4>(c->rec1), m4, dst, evals)
+      P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
 #define CR_THREAD(F, CNT)                                                                     \
   k_composite_thread<F, CNT><<<ntile, kTileSub, 0, str>>>(                                    \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,    \
-      P_<float4>(c->rec0), P_<float4>(c->rec1), m4, dst, evals)
+      P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
   const int fmt = o->output_format;
   if (o->kernel == 0) {
     if (fmt == 0) { if (count) CR_STAGED(0, true); else CR_STAGED(0, false); }

@@ -108,8 +108,8 @@ __device__ __forceinline__ Staged gather_entry(const float4* __restrict__ rec0,
   st.valid = valid;
   if (valid) {
     st.m = mean4[(long long)r - kM];
-    st.r0 = rec0[r];
-    st.r1 = rec1[r];
+    st.r0 = rec0[2ull * r];
+    st.r1 = rec0[2ull * r + 1];
   } else {
     st.m = make_float4(0.f, 0.f, 0.f, 0.f);
     st.r0 = st.m;
@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(kTileSub) k_composite_thread(
     const uint32_t rr = vals[e];
     const float4 m = mean4[(long long)rr - kM];
     const float2 mu = mean2d_fast(cam, m.x, m.y, m.z);
-    const float4 g = rec0[rr];
-    const float4 cl = rec1[rr];
+    const float4 g = rec0[2ull * rr];
+    const float4 cl = rec0[2ull * rr + 1];
     blend_step(g, mu, (&cl.x)[u], px, py, T, C, done);
   }
   if (COUNT) atomicAdd(evals, nev);

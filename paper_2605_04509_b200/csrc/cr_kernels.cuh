@@ -335,8 +335,9 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
 // a4 — Preprocess + SH (Cross-view Coherent Attribute Reuse, Eq.6).
 // One thread per Gaussian, looping over the K clusters so the SH
 // coefficients are read once and evaluated K times.  Per (k,i), r = k*M + i:
-//   rec0[r] = (A', B', C', log2 o)  conic prescaled by -log2(e)/2, -log2(e)
-//   rec1[r] = (r, g, b, ext)        colour at v'_k; ext = half2 (ex, ey) extents
+//   rec[2r]   = (A', B', C', log2 o)  conic prescaled by -log2(e)/2, -log2(e)
+//   rec[2r+1] = (r, g, b, ext)        colour at v'_k; ext = half2 (ex, ey) extents
+//   (one 32-byte aligned record: a composite gather touches one DRAM sector)
 //   geom[2r..2r+1] = exact AccuTile constants (ex, ey, dyR, tc), (1/c, b, det)
 //   dkey[r] = bits(d_{i,k}),  vis[r] = 1 if (i,k) survives culling, else 0
 // ===========================================================================
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(128) k_preprocess(
           geom[2 * r + 1] = make_float4(el.ic, el.b, el.det, 0.0f);
         }
         const float A = c / det, B = -b / det, C = a / det;  // conic (tolerance path)
-        rec0[r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
+        rec0[2 * r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
         // SH colour at the representative camera centre (O11)
         const CamConstDev& cc = c_ccon[jr];
         float dx = m.x - cc.C[0], dy = m.y - cc.C[1], dz = m.z - cc.C[2];
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(128) k_preprocess(
         // subpixel (superfluous cluster-union pairs)
         const float ex = fmaf(sqrtf(tau * a), 1.001f, 0.5f), ey = fmaf(sqrtf(tau * c), 1.001f, 0.5f);
         const __half2 ext = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
-        rec1[r] = make_float4(col[0], col[1], col[2], *reinterpret_cast<const float*>(&ext));
+        rec0[2 * r + 1] = make_float4(col[0], col[1], col[2], *reinterpret_cast<const float*>(&ext));
         dkey[r] = __float_as_uint(p.z);
       }
     }
