@@ -65,11 +65,13 @@ class Stats(C.Structure):
 _lib = None
 
 
-def load(path: str = LIB):
-    """Load the shared library (raises if it was not built)."""
+def load(path: str | None = None):
+    """Load the shared library (raises if it was not built).  CR_LIB overrides
+    the path (A/B timing of alternative builds)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("CR_LIB") or LIB
     if not os.path.exists(path):
         raise ImportError(f"{path} not found: build it with `python -m paper_2605_04509_b200.build` "
                           "(there is no CPU fallback)")

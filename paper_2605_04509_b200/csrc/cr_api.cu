@@ -231,17 +231,20 @@ cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
 // one stable LSD pass
 cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
                      uint32_t* vout, long long n, int shift, bool from_val,
-                     unsigned long long div, bool move_keys) {
+                     unsigned long long div, bool move_keys, bool agg = false) {
   if (n <= 0) return CR_OK;
   const long long nb = (n + kSortTile - 1) / kSortTile;
   CR_TRY(ensure(c, c->hist, (size_t)nb * 256 * 4));
   uint32_t* h = P_<uint32_t>(c->hist);
   if (from_val)
-    k_radix_upsweep<true><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift, div,
-                                                                        h, (int)nb);
+    k_radix_upsweep<true, false><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift,
+                                                                               div, h, (int)nb);
+  else if (agg)
+    k_radix_upsweep<false, true><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift,
+                                                                               div, h, (int)nb);
   else
-    k_radix_upsweep<false><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift, div,
-                                                                         h, (int)nb);
+    k_radix_upsweep<false, false><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(kin, vin, n, shift,
+                                                                                div, h, (int)nb);
   CR_LAUNCHED(c);
   uint32_t* tot = P_<uint32_t>(c->scalars) + 2;
   CR_TRY(dev_scan(c, Scan::InArr{h}, Scan::OutStore{h}, nb * 256, tot));
@@ -725,7 +728,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   int tbits = 1;
   while ((1LL << tbits) < (long long)TX * TY) ++tbits;
   for (int sh = 0; sh < tbits; sh += 8) {
-    CR_TRY(radix_pass(c, tA, pA, tB, pB, P, sh, false, 1, true));
+    // the high tile digit spans only the band's tile rows: aggregate its histogram
+    const bool skewed = sh > 0 && ((long long)(row1 - row0) * TX >> sh) < 64;
+    CR_TRY(radix_pass(c, tA, pA, tB, pB, P, sh, false, 1, true, skewed));
     std::swap(tA, tB);
     std::swap(pA, pB);
   }

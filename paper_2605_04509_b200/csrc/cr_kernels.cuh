@@ -343,6 +343,39 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
 // ===========================================================================
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Conservative band / frame pre-cull of an (i,k) record (exactness-safe): with
+// fast FMA math and a rigorous padding for its rounding (|p_fast - p_exact| <=
+// ~1e-6 (|mu|_1 + |t|_1) per coordinate), decide whether ANY view of cluster
+// k could give the record a tile in the band rows x frame columns.  When this
+// returns false the exact union (O8) is empty, so skipping the record changes
+// no result; when in doubt (near-znear depths) it returns true.
+__device__ __forceinline__ bool may_touch_band(int k, float mx, float my, float mz, float exw,
+                                               float eyw) {
+  const int s = c_fp.s, N = c_fp.N;
+  const int j0 = k * s, j1 = min(j0 + s, N);
+  const float S = fabsf(mx) + fabsf(my) + fabsf(mz);
+  const float ylo = 16.0f * (float)c_fp.row0 - 16.0f, yhi = 16.0f * (float)c_fp.row1 + 16.0f;
+  const float xlo = -16.0f, xhi = 16.0f * (float)c_fp.TX + 16.0f;
+  for (int j = j0; j < j1; ++j) {
+    const CamDev& c = c_cams[j];
+    const float px = fmaf(c.R[0], mx, fmaf(c.R[1], my, fmaf(c.R[2], mz, c.t[0])));
+    const float py = fmaf(c.R[3], mx, fmaf(c.R[4], my, fmaf(c.R[5], mz, c.t[1])));
+    const float pz = fmaf(c.R[6], mx, fmaf(c.R[7], my, fmaf(c.R[8], mz, c.t[2])));
+    const float err = 4e-6f * (S + fabsf(c.t[0]) + fabsf(c.t[1]) + fabsf(c.t[2]) + 1.0f);
+    if (pz + err < c_fp.znear) continue;        // certainly invisible from view j
+    if (pz < 2.0f * c_fp.znear + err) return true;  // too close to call
+    const float iz = 1.0f / pz;
+    const float u = px * iz, v = py * iz;
+    const float ex = c.fx * u + c.cx, ey = c.fy * v + c.cy;
+    const float mgx = c.fx * err * iz * (1.0f + fabsf(u)) * 2.0f + 1e-5f * fabsf(ex) + 1.0f;
+    const float mgy = c.fy * err * iz * (1.0f + fabsf(v)) * 2.0f + 1e-5f * fabsf(ey) + 1.0f;
+    if (ey + eyw + mgy >= ylo && ey - eyw - mgy <= yhi && ex + exw + mgx >= xlo &&
+        ex - exw - mgx <= xhi)
+      return true;
+  }
+  return false;
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
@@ -378,9 +411,14 @@ __global__ void __launch_bounds__(128) k_preprocess(
         if (p.z < c_fp.znear) { vis[r] = 0; ++n_near; continue; }
         float a, b, c, det;
         if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { vis[r] = 0; ++n_deg; continue; }
-        vis[r] = 1;
+        dkey[r] = __float_as_uint(p.z);
         {  // exact per-record AccuTile constants (O7), used by count and emit
           const EllRec el = ell_rec(a, b, c, det, tau);
+          if (!may_touch_band(k, m.x, m.y, m.z, el.ex * 1.001f + 1.0f, el.ey * 1.001f + 1.0f)) {
+            vis[r] = 0;  // no view can reach the band / frame: empty union
+            continue;
+          }
+          vis[r] = 1;
           geom[2 * r] = make_float4(el.ex, el.ey, el.dyR, el.tc);
           geom[2 * r + 1] = make_float4(el.ic, el.b, el.det, 0.0f);
         }
@@ -424,7 +462,6 @@ __global__ void __launch_bounds__(128) k_preprocess(
         const float ex = fmaf(sqrtf(tau * a), 1.001f, 0.5f), ey = fmaf(sqrtf(tau * c), 1.001f, 0.5f);
         const __half2 ext = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
         rec0[2 * r + 1] = make_float4(col[0], col[1], col[2], *reinterpret_cast<const float*>(&ext));
-        dkey[r] = __float_as_uint(p.z);
       }
     }
   }

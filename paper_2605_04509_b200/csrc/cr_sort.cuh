@@ -130,19 +130,34 @@ __device__ __forceinline__ uint32_t sort_digit(const uint32_t* __restrict__ keys
   return (keys[e] >> shift) & 255u;
 }
 
-template <bool DIGIT_FROM_VAL>
+template <bool DIGIT_FROM_VAL, bool AGG>
 __global__ void __launch_bounds__(kSortThreads) k_radix_upsweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, long long n, int shift,
     unsigned long long div, uint32_t* __restrict__ hist /* [256][nb] */, int nb) {
+  // per-warp digit counts.  AGG: equal digits within a round are aggregated
+  // by an 8-ballot multisplit so skewed digit distributions (the few tile
+  // rows of a band in the high tile digit) do not serialise on shared
+  // atomics; otherwise one shared atomic per element (cheaper when spread)
   __shared__ uint32_t s_h[kSortWarps][256];
-  const int w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q = threadIdx.x; q < kSortWarps * 256; q += kSortThreads) (&s_h[0][0])[q] = 0;
   __syncthreads();
   const long long base = (long long)blockIdx.x * kSortTile;
 #pragma unroll 4
   for (int q = 0; q < kSortItems; ++q) {
     const long long e = base + q * kSortThreads + threadIdx.x;
-    if (e < n) atomicAdd(&s_h[w][sort_digit<DIGIT_FROM_VAL>(keys, vals, e, shift, div)], 1u);
+    const uint32_t d = (e < n) ? sort_digit<DIGIT_FROM_VAL>(keys, vals, e, shift, div) : 256u;
+    if (!AGG) {
+      if (d < 256) atomicAdd(&s_h[w][d], 1u);
+      continue;
+    }
+    unsigned peers = __ballot_sync(0xffffffffu, d < 256);
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+      peers &= ((d >> bit) & 1u) ? bal : ~bal;
+    }
+    if (d < 256 && (__ffs(peers) - 1) == lane) atomicAdd(&s_h[w][d], (uint32_t)__popc(peers));
   }
   __syncthreads();
   for (int d = threadIdx.x; d < 256; d += kSortThreads) {

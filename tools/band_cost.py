@@ -1,0 +1,27 @@
+"""Per-rank cost of the row-band split measured on one GPU: render band r of R
+(the work one rank does) and report stage times.  python tools/band_cost.py C 8"""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2605_04509_b200 import CoherentRaster, synthetic as sy
+from paper_2605_04509_b200.multigpu import band_rows
+name = sys.argv[1]; R = int(sys.argv[2])
+c = sy.CONFIGS[name]
+r = CoherentRaster(0)
+r.upload_gaussians(c.make_scene())
+r.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset, c.view_cone)
+r.set_camera_rig(c.make_rig())
+worst = 0
+for q in range(R):
+    rows = band_rows(r.TY, R, q)
+    for _ in range(2):
+        r.render(c.cluster_size, rows=rows, stats=True)
+    ms = []
+    for _ in range(5):
+        r.render(c.cluster_size, rows=rows, stats=True)
+        ms.append(r.last_stats["ms_total"])
+    st = r.last_stats
+    ms.sort()
+    worst = max(worst, ms[2])
+    print(f"band {q}/{R} rows {rows}: total {ms[2]:.2f} ms pre {st['ms_preprocess']:.2f} bin {st['ms_bin']:.2f} sort {st['ms_sort']:.2f} comp {st['ms_composite']:.2f} pairs {st['pairs']}", flush=True)
+print(f"R={R}: slowest band {worst:.2f} ms -> {1000/worst:.1f} frames/s (before the all-gather)")
