@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=None,
                     help="oracle sample: tile rows (default 12 for cpu_baseline, 4 per --impl reference step)")
     ap.add_argument("--ablation", action="store_true", help="also time reuse/remap variants (stderr)")
+    ap.add_argument("--bands", default="balanced", choices=["balanced", "equal"],
+                    help="row-band split for N>1: equal-cost (calibration frame) or equal rows")
     args = ap.parse_args()
 
     from paper_2605_04509_b200 import synthetic as sy
@@ -223,8 +225,14 @@ def main():
     r.set_display(cfg.W, cfg.H, cfg.N, cfg.lens_pitch, cfg.slant, cfg.center_offset, cfg.view_cone)
     r.set_camera_rig(cams)
     TX, TY = r.TX, r.TY
-    from paper_2605_04509_b200.multigpu import BandGather
-    bgt = BandGather(cfg.H, cfg.W, TY, world, rank, dev)
+    from paper_2605_04509_b200.multigpu import BandGather, balanced_bands, row_pair_weights
+    bands = None
+    if world > 1 and args.bands == "balanced":
+        # calibration frame (untimed): per-row pair counts -> equal-cost bands
+        r.render(cfg.cluster_size)
+        torch.cuda.synchronize()
+        bands = balanced_bands(row_pair_weights(r, cfg.cluster_size) + 2.0e5, world)
+    bgt = BandGather(cfg.H, cfg.W, TY, world, rank, dev, bands=bands)
     rows = bgt.rows
     band_out = bgt.out
     remap = not args.no_remap
@@ -342,7 +350,8 @@ def main():
         "config": {"workload": f"config {cfg.name}: {cfg.M} Gaussians SH{cfg.sh_degree} "
                                f"(scene_gen v1), {cfg.N}-view lenticular {cfg.W}x{cfg.H}",
                    "cluster_size": cfg.cluster_size, "remap": remap, "kernel": kernel,
-                   "parallelism": f"row-bands x{world}" if world > 1 else "single",
+                   "parallelism": (f"row-bands x{world} ({args.bands}: {bgt.bands or 'equal rows'})"
+                                   if world > 1 else "single"),
                    "l2": "inputs larger than L2 (scene 0.7 GB, per-frame working set > 3 GB)",
                    "output": "RGB8 interlaced frame in HBM"},
         "pairs": info["pairs"], "visible_ik": info["visible_ik"], "evals": evals,

@@ -21,22 +21,47 @@ def band_rows(TY: int, world: int, rank: int):
     return r0, r0 + base + (1 if rank < extra else 0)
 
 
-def band_pixel_rows(H: int, TY: int, world: int, rank: int):
-    r0, r1 = band_rows(TY, world, rank)
+def balanced_bands(weights, world: int):
+    """Contiguous tile-row bands of ~equal total weight (weights[ty] = cost of
+    tile row ty, e.g. its Gaussian-tile pairs from a calibration frame);
+    every band gets >= 1 row.  Returns [(r0, r1)] * world."""
+    import numpy as np
+    w = np.asarray(weights, np.float64)
+    TY = w.shape[0]
+    if world > TY:
+        raise ValueError("more ranks than tile rows")
+    cum = np.concatenate([[0.0], np.cumsum(np.maximum(w, 0) + 1e-9)])
+    cuts = [0]
+    for q in range(1, world):
+        target = cum[-1] * q / world
+        c = int(np.searchsorted(cum, target))
+        c = max(c, cuts[-1] + 1)           # at least one row per band
+        c = min(c, TY - (world - q))       # leave a row for each later band
+        cuts.append(c)
+    cuts.append(TY)
+    return [(cuts[q], cuts[q + 1]) for q in range(world)]
+
+
+def _pix(H, r0, r1):
     return r0 * 16, min(H, r1 * 16)
 
 
-def padded_band_height(H: int, TY: int, world: int) -> int:
-    return max(band_pixel_rows(H, TY, world, q)[1] - band_pixel_rows(H, TY, world, q)[0]
+def band_pixel_rows(H: int, TY: int, world: int, rank: int, bands=None):
+    r0, r1 = bands[rank] if bands else band_rows(TY, world, rank)
+    return _pix(H, r0, r1)
+
+
+def padded_band_height(H: int, TY: int, world: int, bands=None) -> int:
+    return max(band_pixel_rows(H, TY, world, q, bands)[1] - band_pixel_rows(H, TY, world, q, bands)[0]
                for q in range(world))
 
 
-def assemble(gathered: torch.Tensor, H: int, TY: int, world: int) -> torch.Tensor:
+def assemble(gathered: torch.Tensor, H: int, TY: int, world: int, bands=None) -> torch.Tensor:
     """Full frame [H, W, 3] from the all-gathered padded bands [world*hp, W, 3]."""
     hp = gathered.shape[0] // world
     parts = []
     for q in range(world):
-        y0, y1 = band_pixel_rows(H, TY, world, q)
+        y0, y1 = band_pixel_rows(H, TY, world, q, bands)
         parts.append(gathered[q * hp:q * hp + (y1 - y0)])
     return torch.cat(parts, 0)
 
@@ -44,11 +69,13 @@ def assemble(gathered: torch.Tensor, H: int, TY: int, world: int) -> torch.Tenso
 class BandGather:
     """Preallocated padded band buffer + gather target for one rank."""
 
-    def __init__(self, H: int, W: int, TY: int, world: int, rank: int, device, dtype=torch.uint8):
+    def __init__(self, H: int, W: int, TY: int, world: int, rank: int, device, dtype=torch.uint8,
+                 bands=None):
         self.H, self.W, self.TY, self.world, self.rank = H, W, TY, world, rank
-        self.rows = band_rows(TY, world, rank)
-        y0, y1 = band_pixel_rows(H, TY, world, rank)
-        self.hp = padded_band_height(H, TY, world)
+        self.bands = bands
+        self.rows = bands[rank] if bands else band_rows(TY, world, rank)
+        y0, y1 = band_pixel_rows(H, TY, world, rank, bands)
+        self.hp = padded_band_height(H, TY, world, bands)
         self.band = torch.zeros((self.hp, W, 3), dtype=dtype, device=device)
         self.out = self.band[:y1 - y0]  # what the renderer writes
         self.full = (torch.empty((world * self.hp, W, 3), dtype=dtype, device=device)
@@ -64,7 +91,17 @@ class BandGather:
     def frame(self) -> torch.Tensor:
         if self.world == 1:
             return self.out
-        return assemble(self.full, self.H, self.TY, self.world)
+        return assemble(self.full, self.H, self.TY, self.world, self.bands)
+
+
+def row_pair_weights(renderer, cluster_size: int):
+    """Per-tile-row Gaussian-tile pair counts of the last full-frame render
+    (cr_get_ranges): the load-balancing weights for balanced_bands."""
+    import numpy as np
+    K = -(-renderer.display["num_views"] // cluster_size)
+    S, E = renderer.ranges(K)
+    per_tile = (E.astype(np.int64) - S.astype(np.int64)).sum(axis=1)
+    return per_tile.reshape(renderer.TY, renderer.TX).sum(axis=1)
 
 
 def pose_split(n_poses: int, world: int, rank: int):

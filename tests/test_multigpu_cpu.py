@@ -24,6 +24,21 @@ def test_band_rows_partition():
             assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
 
 
+def test_balanced_bands():
+    rng = np.random.default_rng(0)
+    for TY in (9, 135, 270):
+        w = rng.gamma(0.5, 1.0, TY) * (np.arange(TY) > TY // 3)  # skewed, with empty rows
+        for world in (1, 2, 3, 8):
+            bands = mg.balanced_bands(w, world)
+            assert bands[0][0] == 0 and bands[-1][1] == TY
+            assert all(b[1] > b[0] for b in bands)
+            assert all(bands[q][1] == bands[q + 1][0] for q in range(world - 1))
+            loads = [w[a:b].sum() for a, b in bands]
+            # no band exceeds the ideal share by more than its heaviest single row
+            assert max(loads) <= w.sum() / world + w.max() + 1e-6
+    assert mg.balanced_bands(np.ones(8), 8) == [(q, q + 1) for q in range(8)]
+
+
 def test_pose_split_covers_all():
     got = sorted(sum((mg.pose_split(256, 8, r) for r in range(8)), []))
     assert got == list(range(256)) and len(mg.pose_split(256, 8, 3)) == 32
@@ -43,13 +58,14 @@ def _frame_ref(H, W):
     return ((y * 7 + x * 3 + u * 11) % 251).astype(np.uint8)
 
 
-def _worker(rank, world, port, H, W, q):
+def _worker(rank, world, port, H, W, q, balanced=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     TY = (H + 15) // 16
-    bg = mg.BandGather(H, W, TY, world, rank, "cpu")
+    bands = mg.balanced_bands(np.linspace(0, 1, TY) ** 3, world) if balanced else None
+    bg = mg.BandGather(H, W, TY, world, rank, "cpu", bands=bands)
     ref = _frame_ref(H, W)
-    y0, y1 = mg.band_pixel_rows(H, TY, world, rank)
+    y0, y1 = mg.band_pixel_rows(H, TY, world, rank, bands)
     bg.out.copy_(torch.from_numpy(ref[y0:y1]))  # "render" this rank's band
     bg.gather()
     full = bg.frame().numpy()
@@ -58,13 +74,14 @@ def _worker(rank, world, port, H, W, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("H", [144, 138, 2160])
-def test_gloo_world2_band_gather(H):
+@pytest.mark.parametrize("H,balanced", [(144, False), (138, False), (2160, False), (2160, True)])
+def test_gloo_world2_band_gather(H, balanced):
     W, world = 40, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, q, balanced))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]

@@ -4,16 +4,21 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2605_04509_b200 import CoherentRaster, synthetic as sy
-from paper_2605_04509_b200.multigpu import band_rows
-name = sys.argv[1]; R = int(sys.argv[2])
+from paper_2605_04509_b200.multigpu import band_rows, balanced_bands, row_pair_weights
+name = sys.argv[1]; R = int(sys.argv[2]); mode = sys.argv[3] if len(sys.argv) > 3 else "equal"
 c = sy.CONFIGS[name]
 r = CoherentRaster(0)
 r.upload_gaussians(c.make_scene())
 r.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset, c.view_cone)
 r.set_camera_rig(c.make_rig())
 worst = 0
+bands = None
+if mode == "balanced":
+    r.render(c.cluster_size)
+    torch.cuda.synchronize()
+    bands = balanced_bands(row_pair_weights(r, c.cluster_size) + 2.0e5, R)
 for q in range(R):
-    rows = band_rows(r.TY, R, q)
+    rows = bands[q] if bands else band_rows(r.TY, R, q)
     for _ in range(2):
         r.render(c.cluster_size, rows=rows, stats=True)
     ms = []
