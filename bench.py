@@ -130,6 +130,22 @@ def oracle_sample(cfg, scene, cams, rows, nthreads=0):
             "seconds": dt}
 
 
+def committed_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu table
+    (profiles/r*/ncu_kernels_configC.txt, written by tools/prof_all.sh)."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_kernels_configC.txt")),
+                    reverse=True):
+        for ln in open(f):
+            p = ln.split()
+            if p and p[0].startswith(kernel) and len(p) >= 7:
+                try:  # columns: name.. n time_ms dram_GB GB/s IPC occ%
+                    return float(p[-4]) * 1e9 / int(p[-6]), os.path.relpath(f, ROOT)
+                except ValueError:
+                    pass
+    return None, None
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -336,6 +352,7 @@ def main():
     achieved_tflops = evals * FLOPS_PER_EVAL / (comp_ms * 1e-3) / 1e12 if comp_ms > 0 else None
     peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     bc = compulsory_bytes(cfg, info) if world == 1 else None
+    traffic, traffic_src = committed_traffic("k_composite_staged")
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rows_s = (TY // 2 - args.ref_rows // 2, TY // 2 - args.ref_rows // 2 + args.ref_rows)
@@ -360,7 +377,7 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_composite_staged",
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "note": (f"{FLOPS_PER_EVAL} algorithmic FP32 ops per (subpixel, splat) "
                               f"evaluation x {evals} evaluations / mean composite time; peak = "
                               f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §5)")},

@@ -19,7 +19,7 @@ def val(r, i, unit_row=units):
 agg = collections.OrderedDict()
 for r in rows[2:]:
     n = r[ki].split('(')[0].replace('void ', '').replace('cr::', '')
-    n = n.split('<')[0] + ('<' + r[ki].split('<')[1].split('>')[0] + '>' if '<' in r[ki].split('(')[0] else '')
+    n = n.split('<')[0] + ('<' + r[ki].split('<')[1].split('>')[0].replace(' ', '') + '>' if '<' in r[ki].split('(')[0] else '')
     a = agg.setdefault(n, [0, 0.0, 0.0, 0.0, 0.0, 0.0])
     a[0] += 1; a[1] += val(r, du); a[2] += val(r, dr) + val(r, dw); a[3] += val(r, ipc); a[4] += val(r, occ)
 lt = col('lts__t_bytes.sum')
