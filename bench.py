@@ -30,6 +30,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "interlaced LF frames/s (4K, 100 views)"
+METRICS = {"C": METRIC, "A": "interlaced LF frames/s (256x144, 8 views)",
+           "B": "interlaced LF frames/s (4K, 45 views)", "D": "interlaced LF frames/s (8K, 100 views)",
+           "E": "interlaced LF frames/s (4K, 45 views, 256 head-tracked poses)"}
 UNIT = "frames/s"
 # algorithmic FP32 operations per (subpixel, splat) evaluation of Eqs.9-10
 # (DESIGN.md §5): delta 2, quadratic form 8, x(-1/2) 1, exp 1, o*exp 1,
@@ -178,7 +181,8 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak" if pose_mode else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": f"config {cfg.name}", "gaussians": cfg.M, "sh_degree": cfg.sh_degree,
                    "views": cfg.N, "panel": f"{cfg.W}x{cfg.H}", "cluster_size": cfg.cluster_size,
                    "sample_tile_rows": list(rows)},
@@ -255,7 +259,23 @@ def main():
     kernel = args.kernel if args.kernel is not None else (0 if remap else 1)
     stream = torch.cuda.current_stream(dev)
 
+    pose_mode = cfg.name == "E"
+    if pose_mode:  # config E: head-tracked pose batch split round-robin over ranks
+        from paper_2605_04509_b200.multigpu import pose_split
+        poses = sy.head_tracked_poses(256, seed=1)
+        my_poses = pose_split(len(poses), world, rank)
+        pose_rigs = [cfg.make_rig(**poses[q]) for q in my_poses]
+        rows = None
+        band_out = torch.empty((cfg.H, cfg.W, 3), dtype=torch.uint8, device=dev)
+        pose_i = [0]
+
     def step(stats=False, count=False):
+        if pose_mode:
+            r.set_camera_rig(pose_rigs[pose_i[0] % len(pose_rigs)])
+            pose_i[0] += 1
+            r.render(cfg.cluster_size, remap=remap, kernel=kernel, out=band_out, stats=stats,
+                     count_evals=count)
+            return
         r.render(cfg.cluster_size, remap=remap, kernel=kernel, rows=rows, out=band_out,
                  stats=stats, count_evals=count)
         bgt.gather()
@@ -293,6 +313,8 @@ def main():
     elapsed = float(t.item())
     ms_per = elapsed / args.steps
     fps = args.steps / (elapsed / 1000.0)
+    if pose_mode:
+        fps *= world  # every rank renders its own pose frames
     clocks = clk.summary()
 
     # ---- e2e: public API with host buffers (rig H2D + frame D2H every step)
@@ -301,6 +323,10 @@ def main():
 
     def e2e_step():
         r.set_camera_rig(cams)
+        if pose_mode:
+            step()
+            host.copy_(band_out)
+            return
         if world > 1:
             step()
             host.copy_(bgt.frame())
@@ -320,7 +346,7 @@ def main():
     tw = torch.tensor([w1], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-    e2e_fps = args.steps / float(tw.item())
+    e2e_fps = args.steps / float(tw.item()) * (world if pose_mode else 1)
 
     # ---- ablation (stderr only)
     if args.ablation and rank == 0:
@@ -360,14 +386,15 @@ def main():
         cpu.pop("seconds", None)
         cpu["cpu"] = cpu_model()
     line = {
-        "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRICS.get(cfg.name, METRIC), "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"config {cfg.name}: {cfg.M} Gaussians SH{cfg.sh_degree} "
                                f"(scene_gen v1), {cfg.N}-view lenticular {cfg.W}x{cfg.H}",
                    "cluster_size": cfg.cluster_size, "remap": remap, "kernel": kernel,
-                   "parallelism": (f"row-bands x{world} ({args.bands}: {bgt.bands or 'equal rows'})"
+                   "parallelism": (f"pose batch 256 split x{world}" if pose_mode else
+                                   f"row-bands x{world} ({args.bands}: {bgt.bands or 'equal rows'})"
                                    if world > 1 else "single"),
                    "l2": "inputs larger than L2 (scene 0.7 GB, per-frame working set > 3 GB)",
                    "output": "RGB8 interlaced frame in HBM"},

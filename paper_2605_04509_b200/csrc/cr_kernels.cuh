@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
 // ===========================================================================
 // a6 emit, fast path — one thread per depth-sorted record e decodes the union
 // slot written by k_count and writes <tile, r> at offs[e].  Records flagged
-// in their slot are appended to `elist` for k_emit_groups.
+// in their slot are appended to `elist` for k_emit_big.
 // ===========================================================================
 __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__ rec_sorted,
                                                     const uint32_t* __restrict__ offs, uint32_t n,
