@@ -37,15 +37,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Tolerance-path per-view mean (fast FMA / reciprocal); far away when the
-// view cannot see the Gaussian (Z12) so that alpha underflows to 0.
-__device__ __forceinline__ float2 mean2d_fast(const CamDev& c, float mx, float my, float mz) {
-  const float px = fmaf(c.R[0], mx, fmaf(c.R[1], my, fmaf(c.R[2], mz, c.t[0])));
-  const float py = fmaf(c.R[3], mx, fmaf(c.R[4], my, fmaf(c.R[5], mz, c.t[1])));
-  const float pz = fmaf(c.R[6], mx, fmaf(c.R[7], my, fmaf(c.R[8], mz, c.t[2])));
+// Tolerance-path per-view mean (fast FMA / approximate reciprocal); far away
+// when the view cannot see the Gaussian (Z12) so that alpha underflows to 0.
+// The camera comes as 4 float4 {R0..R3}, {R4..R7}, {R8,t0,t1,t2}, {fx,fy,cx,cy}.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 mean2d_fast4(const float4 a, const float4 b, const float4 c,
+                                               const float4 d, float mx, float my, float mz) {
+  const float px = fmaf(a.x, mx, fmaf(a.y, my, fmaf(a.z, mz, c.y)));
+  const float py = fmaf(a.w, mx, fmaf(b.x, my, fmaf(b.y, mz, c.z)));
+  const float pz = fmaf(b.z, mx, fmaf(b.w, my, fmaf(c.x, mz, c.w)));
   if (!(pz >= c_fp.znear)) return make_float2(1e18f, 1e18f);
-  const float iz = __frcp_rn(pz);
-  return make_float2(fmaf(c.fx, px * iz, c.cx), fmaf(c.fy, py * iz, c.cy));
+  const float iz = rcp_approx(pz);
+  return make_float2(fmaf(d.x, px * iz, d.z), fmaf(d.y, py * iz, d.w));
+}
+__device__ __forceinline__ float2 mean2d_fast(const CamDev& c, float mx, float my, float mz) {
+  const float4* q = reinterpret_cast<const float4*>(&c);
+  return mean2d_fast4(q[0], q[1], q[2], q[3], mx, my, mz);
 }
 
 // One blend step (Eq.10 alpha, Eq.9 accumulation; 0.99 clamp, 1/255 skip,
@@ -136,6 +147,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
   __shared__ float4 s_col[NW][32];
   __shared__ float2 s_mu[NW][kSlots][32];
   __shared__ float4 s_box[NW][kSlots];  // per staged view: pixel box centre, half size
+  __shared__ float4 s_cam4[NW][kSlots][4];  // per staged view: camera (4 float4)
   __shared__ float s_out[kTileSub];
   __shared__ int s_next;
   const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
@@ -209,6 +221,9 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
           s_box[w][v] = make_float4(0.5f * (float)(x0 + x1) + 0.5f, 0.5f * (float)(y0 + y1) + 0.5f,
                                     0.5f * (float)(x1 - x0), 0.5f * (float)(y1 - y0));
       }
+      if (lane < 4 * ns)
+        s_cam4[w][lane >> 2][lane & 3] =
+            reinterpret_cast<const float4*>(&c_cams[jlo + g0 + (lane >> 2)])[lane & 3];
       __syncwarp();
       float T = 1.0f, C = 0.0f;
       bool done = !active;
@@ -230,7 +245,8 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
         }
         unsigned mymask = 0u;
         for (int v = 0; v < ns; ++v) {
-          const float2 mu = mean2d_fast(c_cams[jlo + g0 + v], cur.m.x, cur.m.y, cur.m.z);
+          const float2 mu = mean2d_fast4(s_cam4[w][v][0], s_cam4[w][v][1], s_cam4[w][v][2],
+                                         s_cam4[w][v][3], cur.m.x, cur.m.y, cur.m.z);
           s_mu[w][v][lane] = mu;
           const float4 bx = s_box[w][v];
           const bool pass = cur.valid && fabsf(mu.x - bx.x) <= bx.z + hx &&

@@ -19,7 +19,7 @@ constexpr int kTileSub = kTile * kTile * 3;  // 768 subpixels per tile
 constexpr int kMaxViews = 255;
 constexpr int kMaxCluster = 32;
 
-struct CamDev {
+struct __align__(16) CamDev {
   float R[9], t[3], fx, fy, cx, cy;  // 64 B
 };
 struct CamConstDev {
