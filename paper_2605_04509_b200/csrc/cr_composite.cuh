@@ -66,16 +66,15 @@ __device__ __forceinline__ void blend_step(const float4 g, const float2 m, const
                                            bool& done) {
   const float dx = m.x - px, dy = m.y - py;
   const float q = fmaf(g.x * dx, dx, fmaf(g.z * dy, dy, g.y * dx * dy));  // power*log2(e)
-  if (q <= 0.0f) {
-    const float alpha = fminf(0.99f, ex2_approx(q + g.w));
-    if (alpha >= (1.0f / 255.0f)) {
-      const float Tn = T * (1.0f - alpha);
-      if (Tn < 1e-4f) {
-        done = true;
-      } else {
-        C = fmaf(col, alpha * T, C);
-        T = Tn;
-      }
+  const float a = fminf(0.99f, ex2_approx(q + g.w));
+  const float alpha = (q <= 0.0f) ? a : 0.0f;  // power > 0: skip (folded, one branch)
+  if (alpha >= (1.0f / 255.0f)) {
+    const float Tn = T * (1.0f - alpha);
+    if (Tn < 1e-4f) {
+      done = true;
+    } else {
+      C = fmaf(col, alpha * T, C);
+      T = Tn;
     }
   }
 }
