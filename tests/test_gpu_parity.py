@@ -252,3 +252,86 @@ def test_config_b_full_size_sampled_tiles():
     b = np.concatenate([ref[(t // TX) * 16:(t // TX + 1) * 16, (t % TX) * 16:(t % TX + 1) * 16]
                         for t in tiles])
     assert psnr(np.clip(a, 0, 1), np.clip(b, 0, 1)) >= 50.0
+
+
+def _sampled_tile_check(g, o, cfg, s, tiles, rows=None):
+    TX = (cfg.W + 15) // 16
+    r0, r1 = rows if rows else (0, 0)
+    o.render(s=s, row0=r0, row1=r1, tiles=tiles)
+    img = g.render(s, output_format="float", stats=True, rows=rows).cpu().numpy()
+    st = g.last_stats
+    assert st["pairs"] == int(o.records()["count"].sum())
+    kg, pg = g.sorted_pairs()
+    tg = (kg >> np.uint64(32 + o.bitK)).astype(np.int64)
+    sel = np.isin(tg, tiles)
+    ko, po = o.pairs()
+    assert np.array_equal(kg[sel], ko) and np.array_equal(pg[sel], po)
+    ref = o.image()
+    y0 = r0 * 16
+    a = np.concatenate([img[(t // TX) * 16 - y0:(t // TX + 1) * 16 - y0, (t % TX) * 16:(t % TX + 1) * 16]
+                        for t in tiles])
+    b = np.concatenate([ref[(t // TX) * 16 - y0:(t // TX + 1) * 16 - y0, (t % TX) * 16:(t % TX + 1) * 16]
+                        for t in tiles])
+    assert np.abs(a - b).max() <= 2.0 / 255
+    assert psnr(np.clip(a, 0, 1), np.clip(b, 0, 1)) >= 50.0
+    return st
+
+
+def test_config_c_full_size_sampled_tiles():
+    # the bench workload itself (BASELINE configs[2]: 3M Gaussians SH3, 100 views,
+    # 4K, s=8) in the launch configuration bench.py times: exact pair count, exact
+    # keys/payloads and images on sampled tiles (denser middle rows included)
+    _need_gpu()
+    c = sy.CONFIGS["C"]
+    g, o = make_pair(c.make_scene(), c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset,
+                     c.make_rig())
+    TX, TY = (c.W + 15) // 16, (c.H + 15) // 16
+    rng = np.random.default_rng(1)
+    rows = rng.choice(np.arange(40, 100), 8, replace=False)
+    tiles = np.sort(np.concatenate([rows * TX + rng.integers(0, TX, 8),
+                                    rng.choice(TX * TY, 16, replace=False)])).astype(np.int32)
+    tiles = np.unique(tiles)
+    st = _sampled_tile_check(g, o, c, 8, tiles)
+    assert st["pairs"] > 1e8
+    # a balanced band of the 8-rank split, same checks
+    band = (68, 74)
+    tb = np.unique(np.array([ty * TX + tx for ty in range(*band) for tx in (0, 37, 120, 239)],
+                            np.int32))
+    _sampled_tile_check(g, o, c, 8, tb, rows=band)
+
+
+def test_config_e_head_tracked_pose_sampled_tiles():
+    # BASELINE configs[4]: a head-tracked pose of the 45-view 4K display
+    _need_gpu()
+    c = sy.CONFIGS["E"]
+    pose = sy.head_tracked_poses(256, seed=1)[7]
+    scene = sy.scene_gen_v1(500_000, 3, 0)
+    g, o = make_pair(scene, c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset,
+                     c.make_rig(**pose))
+    TX, TY = (c.W + 15) // 16, (c.H + 15) // 16
+    tiles = np.unique(np.random.default_rng(2).choice(TX * TY, 24, replace=False)).astype(np.int32)
+    _sampled_tile_check(g, o, c, 8, tiles)
+
+
+def test_config_d_8k_sampled_tiles():
+    # BASELINE configs[3] display (7680x4320, 100 views: 17 tile-id bits, 3 tile
+    # radix passes) with a reduced scene so the oracle stays in seconds
+    _need_gpu()
+    c = sy.CONFIGS["D"]
+    scene = sy.scene_gen_v1(600_000, 3, 0)
+    g, o = make_pair(scene, c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset, c.make_rig())
+    TX, TY = (c.W + 15) // 16, (c.H + 15) // 16
+    rng = np.random.default_rng(3)
+    tiles = np.unique(np.concatenate([rng.choice(TX * TY, 16, replace=False),
+                                      (TY // 2) * TX + rng.integers(0, TX, 8)])).astype(np.int32)
+    _sampled_tile_check(g, o, c, 8, tiles)
+
+
+def test_determinism_repeated_frames(cfgA_pair):
+    g, o = cfgA_pair
+    a = g.render(4, output_format="float").cpu().numpy()
+    ka, pa = g.sorted_pairs()
+    for _ in range(3):
+        b = g.render(4, output_format="float").cpu().numpy()
+        kb, pb = g.sorted_pairs()
+        assert np.array_equal(a, b) and np.array_equal(ka, kb) and np.array_equal(pa, pb)
