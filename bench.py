@@ -204,6 +204,7 @@ def main():
     ap.add_argument("--no-remap", action="store_true")
     ap.add_argument("--kernel", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fullframe", action="store_true", help="skip the N1 full-frame comparator")
     ap.add_argument("--ref-rows", type=int, default=None,
                     help="oracle sample: tile rows (default 12 for cpu_baseline, 4 per --impl reference step)")
     ap.add_argument("--ablation", action="store_true", help="also time reuse/remap variants (stderr)")
@@ -348,6 +349,27 @@ def main():
         dist.all_reduce(tw, op=dist.ReduceOp.MAX)
     e2e_fps = args.steps / float(tw.item()) * (world if pose_mode else 1)
 
+    # ---- N1 comparator: full-frame render of every view + interlace
+    ff = None
+    if world == 1 and not args.no_fullframe:
+        mode = dict(cluster_size=1, fullframe=True, remap=True, kernel=0)
+        if pose_mode:
+            r.set_camera_rig(pose_rigs[0])
+        r.render(out=band_out, stats=True, **mode)
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        fe0.record(stream)
+        nff = 3
+        for _ in range(nff):
+            r.render(out=band_out, **mode)
+        fe1.record(stream)
+        torch.cuda.synchronize()
+        ff_ms = fe0.elapsed_time(fe1) / nff
+        ff = {"value": 1000.0 / ff_ms, "unit": UNIT, "ms_per_frame": ff_ms, "frames": nff,
+              "speedup_of_ours": ff_ms / ms_per,
+              "note": "traditional baseline: every view rendered full frame (own attributes, "
+                      "RGB per pixel) then interlaced by V; same kernels' binning/sort"}
+
     # ---- ablation (stderr only)
     if args.ablation and rank == 0:
         for name, s_, rm, kn in [("ours s=8 staged", cfg.cluster_size, True, 0),
@@ -419,6 +441,7 @@ def main():
                         "pinned host memory (wall clock, max over ranks)"},
         "gpu_launches": launches,
         "cpu_baseline": cpu,
+        "fullframe_baseline": ff,
         "scene_gen_s": t_gen,
     }
     print(json.dumps(line), flush=True)

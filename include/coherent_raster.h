@@ -145,7 +145,13 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  *   output_format  0 = RGB8 (floor(clamp(C,0,1)*255+0.5)), 1 = float32
  *   tile_row_begin/end  render only tile rows [begin, end) (row band for
  *                  multi-GPU sharding); 0,0 = full frame
- *   flags          CR_FLAG_COUNT_EVALS counts (subpixel, splat) evaluations
+ *   flags          CR_FLAG_COUNT_EVALS counts (subpixel, splat) evaluations;
+ *                  CR_FLAG_FULLFRAME renders the traditional baseline instead
+ *                  (SURVEY N1): every one of the N views at full
+ *                  resolution with its own attributes (cluster_size must be
+ *                  1), one RGB pixel per thread, into an internal
+ *                  [N][rows][W][3] buffer, then interlaced by V.
+ *                  Equal, subpixel by subpixel, to the s=1 subpixel path.
  * out: caller-owned, [rows][W][3] of the band (rows = clipped band height),
  * out_bytes must be >= rows*W*3*(1 or 4).  out_on_device selects a device
  * pointer (written on the stream) or a host pointer (copied back, the call
@@ -153,6 +159,7 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  * and fills it.
  * ------------------------------------------------------------------- */
 #define CR_FLAG_COUNT_EVALS 1
+#define CR_FLAG_FULLFRAME 2
 typedef struct {
   int32_t cluster_size;
   int32_t remap;

@@ -107,7 +107,7 @@ struct cr_ctx {
   DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, vlist, slots, elist, biglist;
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
-  DevBuf bsum, hist, scalars, S, E, stage_out;
+  DevBuf bsum, hist, scalars, S, E, stage_out, frames;
   DevBuf tmp;                      // upload staging
   uint32_t* h_pinned = nullptr;    // small pinned readback
   // last frame
@@ -352,7 +352,7 @@ void cr_destroy(cr_ctx* c) {
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
                    &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist,
-                   &c->scalars, &c->S, &c->E, &c->stage_out, &c->tmp};
+                   &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -532,6 +532,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (o->kernel == 0 && o->remap == 0)
     return fail(c, CR_ERR_INVALID_ARG, "the staged composite needs remap=1 (use kernel=1)");
   if (o->output_format != 0 && o->output_format != 1) return fail(c, CR_ERR_INVALID_ARG, "format");
+  const bool fullframe = (o->flags & CR_FLAG_FULLFRAME) != 0;
+  if (fullframe && s != 1)
+    return fail(c, CR_ERR_INVALID_CONFIG, "the full-frame baseline renders every view: cluster_size must be 1");
   for (int u = 0; u < 3; ++u)
     if (!std::isfinite(o->background[u])) return fail(c, CR_ERR_NONFINITE, "background");
   int row0 = o->tile_row_begin, row1 = o->tile_row_end;
@@ -574,7 +577,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_fp, &fp, sizeof(fp), 0, cudaMemcpyHostToDevice, str));
 
   // ---- composite work items (static per display and s)
-  if (o->kernel == 0 && c->chunks_s != s) {
+  if (o->kernel == 0 && !fullframe && c->chunks_s != s) {
     const int stride = K + 24;
     CR_TRY(ensure(c, c->chunks, (size_t)TX * TY * stride * 4));
     CR_TRY(ensure(c, c->nchunks, (size_t)TX * TY * 4));
@@ -766,7 +769,22 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,    \
       P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
   const int fmt = o->output_format;
-  if (o->kernel == 0) {
+  if (fullframe) {
+    const size_t fb = (size_t)N * (y1 - y0) * W * 3 * (fmt ? 4 : 1);
+    CR_TRY(ensure(c, c->frames, fb));
+    const unsigned nb = ntile * (unsigned)N;
+    if (fmt == 0)
+      k_fullframe<0><<<nb, 256, 0, str>>>(P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,
+                                          P_<float4>(c->rec0), m4, c->frames.p);
+    else
+      k_fullframe<1><<<nb, 256, 0, str>>>(P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,
+                                          P_<float4>(c->rec0), m4, c->frames.p);
+    CR_LAUNCHED(c);
+    const long long nsub = (long long)(y1 - y0) * W * 3;
+    const unsigned gi = (unsigned)std::min<long long>(grid_for(nsub, 256), 148 * 32);
+    if (fmt == 0) k_interlace<0><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
+    else k_interlace<1><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
+  } else if (o->kernel == 0) {
     if (fmt == 0) { if (count) CR_STAGED(0, true); else CR_STAGED(0, false); }
     else          { if (count) CR_STAGED(1, true); else CR_STAGED(1, false); }
   } else {

@@ -282,6 +282,89 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
   store_tile<FMT>(s_out, out, tx, ty, W, H, c_fp.row0 * 16);
 }
 
+// ===========================================================================
+// N1 baseline: full-frame 3DGS of every view, then interlace.
+// CTA = (tile, view j): 256 threads = the tile's pixels, RGB per thread; list
+// (t, j) of the s=1 binning; entries staged in shared memory 256 at a time
+// with their view-j mean; a CTA-wide count ends the list when all pixels
+// saturate.  Each channel uses exactly the staged kernel's blend arithmetic,
+// so interlacing the frames reproduces the s=1 subpixel render bit for bit.
+// ===========================================================================
+template <int FMT>
+__global__ void __launch_bounds__(256) k_fullframe(const uint32_t* __restrict__ S,
+                                                   const uint32_t* __restrict__ E,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const float4* __restrict__ rec,
+                                                   const float4* __restrict__ mean4,
+                                                   void* __restrict__ frames) {
+  __shared__ float4 s_g[256];
+  __shared__ float4 s_c[256];
+  __shared__ float2 s_m[256];
+  const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
+  const long long M = c_fp.M;
+  const int t = c_fp.row0 * TX + (int)(blockIdx.x % (unsigned)((c_fp.row1 - c_fp.row0) * TX));
+  const int j = (int)(blockIdx.x / (unsigned)((c_fp.row1 - c_fp.row0) * TX));
+  const int tx = t % TX, ty = t / TX;
+  const int x = tx * 16 + (threadIdx.x & 15), y = ty * 16 + (threadIdx.x >> 4);
+  const bool inside = x < W && y < H;
+  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const int k = j;  // s = 1: every view is its own cluster
+  const uint32_t e0 = S[t * K + k], e1 = E[t * K + k];
+  const long long kM = (long long)k * M;
+  const CamDev& cam = c_cams[j];
+  float T[3] = {1.f, 1.f, 1.f}, C[3] = {0.f, 0.f, 0.f};
+  bool done[3] = {!inside, !inside, !inside};
+  for (uint32_t b = e0; b < e1; b += 256) {
+    __syncthreads();
+    const uint32_t e = b + threadIdx.x;
+    if (e < e1) {
+      const uint32_t r = vals[e];
+      const float4 m = mean4[(long long)r - kM];
+      s_g[threadIdx.x] = rec[2ull * r];
+      s_c[threadIdx.x] = rec[2ull * r + 1];
+      s_m[threadIdx.x] = mean2d_fast(cam, m.x, m.y, m.z);
+    }
+    __syncthreads();
+    const int n = (int)min(256u, e1 - b);
+    for (int q = 0; q < n && !(done[0] && done[1] && done[2]); ++q) {
+      const float4 g = s_g[q];
+      const float2 mu = s_m[q];
+      const float4 cl = s_c[q];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (!done[u]) blend_step(g, mu, (&cl.x)[u], px, py, T[u], C[u], done[u]);
+    }
+    if (__syncthreads_count(done[0] && done[1] && done[2]) == 256) break;
+  }
+  if (!inside) return;
+  const long long o = ((((long long)j * (c_fp.row1 - c_fp.row0) * 16 + (y - c_fp.row0 * 16)) * W) + x) * 3;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const float v = C[u] + c_fp.bg[u] * T[u];
+    if (FMT == 0) {
+      const float cl = fminf(fmaxf(v, 0.0f), 1.0f);
+      ((uint8_t*)frames)[o + u] = (uint8_t)floorf(__fadd_rn(__fmul_rn(cl, 255.0f), 0.5f));
+    } else {
+      ((float*)frames)[o + u] = v;
+    }
+  }
+}
+
+// interlace: out[y][x][u] = F_{V[y][x][u]}[y][x][u] for the band
+template <int FMT>
+__global__ void k_interlace(const uint8_t* __restrict__ V, const void* __restrict__ frames,
+                            void* __restrict__ out, int rows_px) {
+  const long long n = (long long)rows_px * c_fp.W * 3;
+  const long long plane = n;
+  const long long base = (long long)c_fp.row0 * 16 * c_fp.W * 3;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int j = V[base + q];
+    if (FMT == 0) ((uint8_t*)out)[q] = ((const uint8_t*)frames)[(long long)j * plane + q];
+    else ((float*)out)[q] = ((const float*)frames)[(long long)j * plane + q];
+  }
+}
+
 template <int FMT, bool COUNT>
 __global__ void __launch_bounds__(kTileSub) k_composite_thread(
     const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,

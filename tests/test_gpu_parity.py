@@ -335,3 +335,21 @@ def test_determinism_repeated_frames(cfgA_pair):
         b = g.render(4, output_format="float").cpu().numpy()
         kb, pb = g.sorted_pairs()
         assert np.array_equal(a, b) and np.array_equal(ka, kb) and np.array_equal(pa, pb)
+
+
+def test_fullframe_baseline_equals_subpixel_s1(cfgA_pair):
+    # N1: rendering every view full frame and interlacing by V gives,
+    # subpixel by subpixel, the s=1 subpixel render (same lists, same blend ops),
+    # and matches the oracle's brute force (full frame per view + interlace).
+    g, o = cfgA_pair
+    sub = g.render(1, output_format="float").cpu().numpy()
+    ff = g.render(1, output_format="float", fullframe=True, stats=True).cpu().numpy()
+    assert np.array_equal(sub, ff)
+    o.render(s=1)
+    bf = o.bruteforce()
+    assert np.abs(ff - bf).max() <= 2.0 / 255 and psnr(np.clip(ff, 0, 1), np.clip(bf, 0, 1)) >= 50
+    band = g.render(1, output_format="rgb8", fullframe=True, rows=(2, 6)).cpu().numpy()
+    assert np.array_equal(band, g.render(1, output_format="rgb8", rows=(2, 6)).cpu().numpy())
+    from paper_2605_04509_b200._native import CrError
+    with pytest.raises(CrError, match="INVALID_CONFIG"):
+        g.render(8, fullframe=True)
