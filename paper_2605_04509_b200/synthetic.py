@@ -265,6 +265,14 @@ CONFIGS = {
                 "scene_gen_v1", 0, gpus=8),
     "E": Config("E", 3_000_000, 3, 45, 3840, 2160, 19.6153, _SLANT_LG, 7.3, 53.0, 8,
                 "scene_gen_v1", 0, gpus=8),
+    # the paper's own display setups on the
+    # 3M-Gaussian synthetic scene: 63-view 1440x2560 portrait (s=16) and
+    # 71-view 3840x2160 landscape (s=18); lens parameters are unpublished
+    # (S:206), so the Looking-Glass-style values above are reused.
+    "P2K": Config("P2K", 3_000_000, 3, 63, 1440, 2560, 19.6153, _SLANT_LG, 7.3, 53.0, 16,
+                  "scene_gen_v1", 0),
+    "P4K": Config("P4K", 3_000_000, 3, 71, 3840, 2160, 19.6153, _SLANT_LG, 7.3, 53.0, 18,
+                  "scene_gen_v1", 0),
 }
 
 
