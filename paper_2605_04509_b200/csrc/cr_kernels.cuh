@@ -511,6 +511,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
   __shared__ float s_cam[kMaxViews * kCamStride];
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
+  __shared__ int s_src[kBinWarps][32];  // item-window position -> source lane
   stage_cams(s_cam);
   __syncthreads();
   constexpr int GPW = 32 / G;  // groups (records) per warp
@@ -579,13 +580,17 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
     __syncwarp();
     // ---- (view, row) items, 32 per window: lane i takes item base+i
     for (int base = 0; base < total; base += 32) {
+      // source lane of item base+lane: the lane whose item segment starts at the
+      // last segment start <= this window position (starts marked in s_src)
       const bool inter = ni > 0 && pre > base && seg0 < base + 32;
-      const unsigned ib = __ballot_sync(0xffffffffu, inter);
-      const unsigned marks = __reduce_or_sync(0xffffffffu, inter ? (1u << (max(seg0, base) - base)) : 0u);
+      const int spos = max(seg0, base) - base;
+      if (inter) s_src[w][spos] = lane;
+      const unsigned marks = __reduce_or_sync(0xffffffffu, inter ? (1u << spos) : 0u);
       const int idx = base + lane;
       const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-      const int kk = __popc(marks & upto);
-      const int src = (idx < total && kk > 0) ? (int)__fns(ib, 0, kk) : 0;
+      const unsigned mk = marks & upto;
+      __syncwarp();
+      const int src = (idx < total && mk) ? s_src[w][31 - __clz(mk)] : 0;
       const float smx = __shfl_sync(0xffffffffu, mx, src);
       const float smy = __shfl_sync(0xffffffffu, my, src);
       const int sfirst = __shfl_sync(0xffffffffu, first, src);
