@@ -233,10 +233,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CR_BENCH_BACKEND=gloo (testing only): run N ranks on fewer GPUs through gloo
+    backend = os.environ.get("CR_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     t_gen = time.perf_counter()
     scene, cams = cfg.make_scene(), cfg.make_rig()
@@ -421,7 +427,7 @@ def main():
                    "l2": "inputs larger than L2 (scene 0.7 GB, per-frame working set > 3 GB)",
                    "output": "RGB8 interlaced frame in HBM"},
         "pairs": info["pairs"], "visible_ik": info["visible_ik"], "evals": evals,
-        "mean_traversal": evals / (cfg.W * cfg.H * 3),
+        "mean_traversal": evals / max(1, band_out.numel()),  # rank 0's band
         "stage_ms": {k: v / args.steps for k, v in ms_stage.items()},
         "roofline": {"bound": "alu", "kernel": "k_composite_staged",
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",

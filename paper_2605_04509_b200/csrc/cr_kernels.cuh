@@ -364,7 +364,7 @@ __device__ __forceinline__ bool may_touch_band(int k, float mx, float my, float 
     const float err = 4e-6f * (S + fabsf(c.t[0]) + fabsf(c.t[1]) + fabsf(c.t[2]) + 1.0f);
     if (pz + err < c_fp.znear) continue;        // certainly invisible from view j
     if (pz < 2.0f * c_fp.znear + err) return true;  // too close to call
-    const float iz = 1.0f / pz;
+    const float iz = __fdividef(1.0f, pz);  // approximate: covered by the padding
     const float u = px * iz, v = py * iz;
     const float ex = c.fx * u + c.cx, ey = c.fy * v + c.cy;
     const float mgx = c.fx * err * iz * (1.0f + fabsf(u)) * 2.0f + 1e-5f * fabsf(ex) + 1.0f;

@@ -85,7 +85,12 @@ class BandGather:
         """All-gather the padded bands; returns the padded stack (or the band at world 1)."""
         if self.world == 1:
             return self.band
-        dist.all_gather_into_tensor(self.full, self.band, group=group)
+        if dist.get_backend(group) == "nccl" or self.band.device.type == "cpu":
+            dist.all_gather_into_tensor(self.full, self.band, group=group)
+        else:  # gloo with CUDA tensors (tests): list all_gather through host copies
+            parts = [torch.empty_like(self.band, device="cpu") for _ in range(self.world)]
+            dist.all_gather(parts, self.band.cpu(), group=group)
+            self.full.copy_(torch.cat(parts, 0))
         return self.full
 
     def frame(self) -> torch.Tensor:
