@@ -56,13 +56,25 @@ struct Scan {  // functors for the generic device scan
     const uint32_t* list;
     __device__ uint32_t operator()(long long e) const { return cnt[list[e]] > 0u ? 1u : 0u; }
   };
-  struct OutCompactList {
+  struct OutCompactList {  // presort key: (k << B) | (depth bits - dmin) when it fits 32 bits
     const uint32_t* list;
     const uint32_t* dkey;
     uint32_t* ko;
     uint32_t* vo;
+    const uint32_t* drange;
+    int kbits;
     __device__ void operator()(long long e, uint32_t ex, uint32_t v) const {
-      if (v) { const uint32_t r = list[e]; ko[ex] = dkey[r]; vo[ex] = r; }
+      if (!v) return;
+      const uint32_t r = list[e];
+      const uint32_t d = dkey[r], lo = drange[0], span = drange[1] - lo;
+      const int B = span ? 32 - __clz(span) : 1;
+      uint32_t key = d;
+      if (B + kbits <= 32) {
+        key = d - lo;
+        if (kbits) key |= fdiv(r, c_fp.divM) << B;
+      }
+      ko[ex] = key;
+      vo[ex] = r;
     }
   };
   struct InGather {
@@ -261,6 +273,13 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
   return CR_OK;
 }
 
+cr_status read_words(cr_ctx* c, const uint32_t* d, uint32_t* h, int n) {
+  CR_CUDA(c, cudaMemcpyAsync(c->h_pinned, d, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  CR_CUDA(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(h, c->h_pinned, 4 * n);
+  return CR_OK;
+}
+
 cr_status read_u32(cr_ctx* c, const uint32_t* d, uint32_t* h) {
   CR_CUDA(c, cudaMemcpyAsync(c->h_pinned, d, 4, cudaMemcpyDeviceToHost, c->stream));
   CR_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -332,7 +351,7 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
     signal(SIGBUS, segv_handler);
   }
   c->stream = (cudaStream_t)cuda_stream;
-  if (cudaSetDevice(cuda_device) != cudaSuccess || cudaMallocHost(&c->h_pinned, 64) != cudaSuccess) {
+  if (cudaSetDevice(cuda_device) != cudaSuccess || cudaMallocHost(&c->h_pinned, 256) != cudaSuccess) {
     delete c;
     return CR_ERR_CUDA;
   }
@@ -593,6 +612,8 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   // counters: [0] near [1] degenerate [2] opacity [3] evals (u64 at byte 32)
   unsigned long long* counters = (unsigned long long*)(sc + 8);
   CR_CUDA(c, cudaMemsetAsync(sc, 0, 64, str));
+  CR_CUDA(c, cudaMemsetAsync(sc + 16, 0xFF, 4, str));  // depth-bit range [min, max]
+  CR_CUDA(c, cudaMemsetAsync(sc + 17, 0, 4, str));
   CR_TRACE(c, "constants+chunks");
   CR_CUDA(c, cudaEventRecord(c->ev[0], str));
 
@@ -616,13 +637,16 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
   uint32_t nvis = 0, nvis0 = 0;
+  uint32_t drange_h[2] = {0u, 0u};
+  int kbits = 0;  // bits of the cluster id in the compressed presort key
+  while ((1 << kbits) < K) ++kbits;
   if (M > 0) {
     const unsigned g = grid_for(M, 128);
 #define CR_PRE(D)                                                                               \
   k_preprocess<D><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
                                       P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
                                       P_<float4>(c->rec0) + 1, P_<float4>(c->geom),                 \
-                                      P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters)
+                                      P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters, sc + 16)
     switch (c->deg) {
       case 0: CR_PRE(0); break;
       case 1: CR_PRE(1); break;
@@ -661,9 +685,14 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       // records with >= 1 tile in the band -> (depth key, r)
       CR_TRY(dev_scan(c, Scan::InCntPos{P_<uint32_t>(c->cnt), P_<uint32_t>(c->vlist)},
                       Scan::OutCompactList{P_<uint32_t>(c->vlist), P_<uint32_t>(c->dkey),
-                                           P_<uint32_t>(c->ka), P_<uint32_t>(c->va)},
+                                           P_<uint32_t>(c->ka), P_<uint32_t>(c->va), sc + 16,
+                                           kbits},
                       nvis0, sc + 0));
-      CR_TRY(read_u32(c, sc + 0, &nvis));
+      uint32_t hw[18];
+      CR_TRY(read_words(c, sc, hw, 18));  // nvis and the depth-bit range in one read
+      nvis = hw[0];
+      drange_h[0] = hw[16];
+      drange_h[1] = hw[17];
     }
     CR_TRACE(c, "compaction");
   }
@@ -672,12 +701,20 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   // ---- a7 depth presort: stable by depth bits (4 passes), then by k (1 pass)
   uint32_t *kA = P_<uint32_t>(c->ka), *vA = P_<uint32_t>(c->va);
   uint32_t *kB = P_<uint32_t>(c->kb), *vB = P_<uint32_t>(c->vb);
-  for (int pass = 0; pass < 4; ++pass) {
-    CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, 8 * pass, false, 1, true));
+  int key_bits = 32;
+  bool compressed = false;
+  if (nvis > 0) {
+    const uint32_t span = drange_h[1] - drange_h[0];
+    int B = 1;
+    while (B < 32 && (span >> B)) ++B;
+    if (B + kbits <= 32) { compressed = true; key_bits = B + kbits; }
+  }
+  for (int sh = 0; sh < key_bits; sh += 8) {
+    CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, sh, false, 1, true));
     std::swap(kA, kB);
     std::swap(vA, vB);
   }
-  if (K > 1) {
+  if (!compressed && K > 1) {  // key did not fit: stable cluster pass on top
     CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, 0, true, (unsigned long long)M, false));
     std::swap(vA, vB);
   }
@@ -743,7 +780,8 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_CUDA(c, cudaMemsetAsync(c->S.p, 0, nSE * 4, str));
   CR_CUDA(c, cudaMemsetAsync(c->E.p, 0, nSE * 4, str));
   if (P > 0) {
-    k_ranges<<<grid_for(P, 256), 256, 0, str>>>(tA, pA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
+    k_ranges<<<(unsigned)std::min<long long>(grid_for((P + 3) / 4, 256), 148 * 8), 256, 0, str>>>(
+        tA, pA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
     CR_LAUNCHED(c);
   }
   CR_TRACE(c, "tile sort+ranges");

@@ -381,11 +381,13 @@ __global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
     const float* __restrict__ shsoa, float4* __restrict__ rec0, float4* __restrict__ rec1,
     float4* __restrict__ geom, uint32_t* __restrict__ dkey, uint32_t* __restrict__ vis,
-    unsigned long long* __restrict__ counters /* near, degenerate, opacity */) {
+    unsigned long long* __restrict__ counters /* near, degenerate, opacity */,
+    uint32_t* __restrict__ drange /* [min, max] depth bits of kept records */) {
   constexpr int NC = (DEG + 1) * (DEG + 1);
   const long long M = c_fp.M;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   unsigned n_near = 0, n_deg = 0, n_op = 0;
+  uint32_t dmn = 0xFFFFFFFFu, dmx = 0u;
   if (i < M) {
     const float4 m = mean4[i];
     const float tau = m.w;
@@ -419,6 +421,8 @@ __global__ void __launch_bounds__(128) k_preprocess(
             continue;
           }
           vis[r] = 1;
+          dmn = min(dmn, __float_as_uint(p.z));
+          dmx = max(dmx, __float_as_uint(p.z));
           geom[2 * r] = make_float4(el.ex, el.ey, el.dyR, el.tc);
           geom[2 * r + 1] = make_float4(el.ic, el.b, el.det, 0.0f);
         }
@@ -474,6 +478,13 @@ __global__ void __launch_bounds__(128) k_preprocess(
   if (n_op) atomicAdd(&s_c[2], n_op);
   __syncthreads();
   if (threadIdx.x < 3 && s_c[threadIdx.x]) atomicAdd(&counters[threadIdx.x], s_c[threadIdx.x]);
+  // depth-bit range of the kept records (the presort compresses its keys to it)
+  dmn = __reduce_min_sync(0xffffffffu, dmn);
+  dmx = __reduce_max_sync(0xffffffffu, dmx);
+  if ((threadIdx.x & 31) == 0 && dmx >= dmn) {
+    atomicMin(&drange[0], dmn);
+    atomicMax(&drange[1], dmx);
+  }
 }
 
 // ===========================================================================
@@ -774,22 +785,45 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
 // ===========================================================================
 // a8 — ranges [S_{t,k}, E_{t,k}) from the (t, k)-sorted pairs.
 // ===========================================================================
-__global__ void k_ranges(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ val,
-                         uint32_t P, uint32_t* __restrict__ S, uint32_t* __restrict__ E) {
-  // one load of (t, k) per element; neighbours via shuffles (lanes 0/31 load
-  // their outer neighbour once)
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ tkey,
+                                                const uint32_t* __restrict__ val, uint32_t P,
+                                                uint32_t* __restrict__ S, uint32_t* __restrict__ E) {
+  // 4 consecutive pairs per thread (16-byte loads), grid-stride over quads;
+  // (t, k) slot keys of the neighbours via shuffles, lanes 0/31 load their
+  // outer neighbour once.  Buffers are padded, so a partial last quad is safe.
   const int lane = threadIdx.x & 31;
-  const int K = c_fp.K;
-  uint32_t key = 0xFFFFFFFFu;
-  if (e < P) key = tkey[e] * (uint32_t)K + fdiv(val[e], c_fp.divM);  // slot t*K + k
-  uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-  uint32_t next = __shfl_down_sync(0xffffffffu, key, 1);
-  if (lane == 0) prev = (e > 0 && e < P) ? tkey[e - 1] * (uint32_t)K + fdiv(val[e - 1], c_fp.divM) : 0xFFFFFFFEu;
-  if (lane == 31) next = (e + 1 < P) ? tkey[e + 1] * (uint32_t)K + fdiv(val[e + 1], c_fp.divM) : 0xFFFFFFFEu;
-  if (e >= P) return;
-  if (e == 0 || prev != key) S[key] = e;
-  if (e == P - 1 || next != key) E[key] = e + 1;
+  const uint32_t K = (uint32_t)c_fp.K;
+  const uint32_t nq = (P + 3) / 4;
+  auto slot_of = [&](uint32_t e) -> uint32_t {
+    return tkey[e] * K + fdiv(val[e], c_fp.divM);
+  };
+  for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < nq; q0 += gridDim.x * blockDim.x) {
+    const uint32_t q = q0 + threadIdx.x;
+    const uint32_t e = 4 * q;
+    uint32_t key[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (q < nq) {
+      const uint4 tt = reinterpret_cast<const uint4*>(tkey)[q];
+      const uint4 vv = reinterpret_cast<const uint4*>(val)[q];
+      const uint32_t ta[4] = {tt.x, tt.y, tt.z, tt.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        if (e + h < P) key[h] = ta[h] * K + fdiv(va[h], c_fp.divM);
+    }
+    uint32_t prev = __shfl_up_sync(0xffffffffu, key[3], 1);
+    uint32_t next = __shfl_down_sync(0xffffffffu, key[0], 1);
+    if (lane == 0) prev = (q < nq && e > 0) ? slot_of(e - 1) : 0xFFFFFFFEu;
+    if (lane == 31) next = (q < nq && e + 4 < P) ? slot_of(e + 4) : 0xFFFFFFFEu;
+    if (q >= nq) continue;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t eh = e + h;
+      if (eh >= P) break;
+      const uint32_t pk = h == 0 ? prev : key[h - 1];
+      const uint32_t nk = (h == 3 || eh + 1 >= P) ? (h == 3 ? next : 0xFFFFFFFEu) : key[h + 1];
+      if (eh == 0 || pk != key[h]) S[key[h]] = eh;
+      if (eh == P - 1 || nk != key[h]) E[key[h]] = eh + 1;
+    }
+  }
 }
 
 // Introspection: 64-bit keys of Eq.11 and payload i.
