@@ -120,6 +120,8 @@ struct cr_ctx {
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
   DevBuf bsum, hist, scalars, S, E, stage_out, frames;
+  DevBuf look;                     // onesweep look-back status words
+  uint32_t epoch = 0;              // look-back tag of the last radix pass
   DevBuf tmp;                      // upload staging
   uint32_t* h_pinned = nullptr;    // small pinned readback
   // last frame
@@ -273,6 +275,46 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
   return CR_OK;
 }
 
+// Stable LSD sort of (key, value) pairs on key bits [shift0, shift0 + 8*npass)
+// by onesweep passes (one histogram kernel + one kernel per digit).  The
+// result lands in (kA, vA) after the swaps (the pointers are swapped here).
+// aggmask bit p: digit p is skewed (band mode), aggregate its histogram.
+constexpr int kOneItems = 16;
+cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uint32_t*& vB,
+                     long long n, int shift0, int npass, unsigned aggmask = 0) {
+  if (n <= 0 || npass <= 0) return CR_OK;
+  if (npass > 4) return fail(c, CR_ERR_CAPACITY, "radix_sort: npass %d > 4", npass);
+  constexpr long long kTile = (long long)kSortThreads * kOneItems;
+  const long long nb = (n + kTile - 1) / kTile;
+  CR_TRY(ensure(c, c->hist, (size_t)(4 * 256 + 16) * 4));
+  const size_t lbytes = (size_t)nb * 256 * 8;
+  if (lbytes > c->look.bytes || !c->look.p) {
+    CR_TRY(ensure(c, c->look, lbytes));
+    CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
+    c->epoch = 0;
+  }
+  uint32_t* gh = P_<uint32_t>(c->hist);
+  uint32_t* ctr = gh + 4 * 256;
+  CR_CUDA(c, cudaMemsetAsync(gh, 0, (4 * 256 + 16) * 4, c->stream));
+  const unsigned hgrid = (unsigned)std::max<long long>(
+      1, std::min<long long>((n / 4 + kHistThreads - 1) / kHistThreads, 148 * 8));
+  k_radix_hist<<<hgrid, kHistThreads, 0, c->stream>>>(kA, n, shift0, npass, aggmask, gh);
+  CR_LAUNCHED(c);
+  for (int p = 0; p < npass; ++p) {
+    if (++c->epoch >= (1u << 30)) {  // never in practice; keep the tags unambiguous
+      CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
+      c->epoch = 1;
+    }
+    k_radix_onesweep<kOneItems><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+        kA, vA, kB, vB, n, shift0 + 8 * p, gh + 256 * p, P_<unsigned long long>(c->look),
+        ctr + p, c->epoch);
+    CR_LAUNCHED(c);
+    std::swap(kA, kB);
+    std::swap(vA, vB);
+  }
+  return CR_OK;
+}
+
 cr_status read_words(cr_ctx* c, const uint32_t* d, uint32_t* h, int n) {
   CR_CUDA(c, cudaMemcpyAsync(c->h_pinned, d, 4 * n, cudaMemcpyDeviceToHost, c->stream));
   CR_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -370,7 +412,7 @@ void cr_destroy(cr_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
                    &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
-                   &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist,
+                   &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist, &c->look,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)
@@ -709,11 +751,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     while (B < 32 && (span >> B)) ++B;
     if (B + kbits <= 32) { compressed = true; key_bits = B + kbits; }
   }
-  for (int sh = 0; sh < key_bits; sh += 8) {
-    CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, sh, false, 1, true));
-    std::swap(kA, kB);
-    std::swap(vA, vB);
-  }
+  CR_TRY(radix_sort(c, kA, vA, kB, vB, nvis, 0, (key_bits + 7) / 8));
   if (!compressed && K > 1) {  // key did not fit: stable cluster pass on top
     CR_TRY(radix_pass(c, kA, vA, kB, vB, nvis, 0, true, (unsigned long long)M, false));
     std::swap(vA, vB);
@@ -767,12 +805,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   // ---- a7 stable tile sort + a8 ranges
   int tbits = 1;
   while ((1LL << tbits) < (long long)TX * TY) ++tbits;
-  for (int sh = 0; sh < tbits; sh += 8) {
-    // the high tile digit spans only the band's tile rows: aggregate its histogram
-    const bool skewed = sh > 0 && ((long long)(row1 - row0) * TX >> sh) < 64;
-    CR_TRY(radix_pass(c, tA, pA, tB, pB, P, sh, false, 1, true, skewed));
-    std::swap(tA, tB);
-    std::swap(pA, pB);
+  {
+    // digits that span only the band's few tile rows: aggregate their histograms
+    unsigned agg = 0;
+    for (int sh = 8, q = 1; sh < tbits; sh += 8, ++q)
+      if (((long long)(row1 - row0) * TX >> sh) < 64) agg |= 1u << q;
+    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, (tbits + 7) / 8, agg));
   }
   const size_t nSE = (size_t)TX * TY * K;
   CR_TRY(ensure(c, c->S, nSE * 4));

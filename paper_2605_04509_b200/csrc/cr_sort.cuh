@@ -271,4 +271,211 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_downsweep(
   }
 }
 
+// ------------------------------------------------------ onesweep radix
+// Single-pass-per-digit variant (decoupled look-back): one histogram kernel
+// reads the keys once for all digit positions, then each pass is ONE kernel
+// whose blocks take their tile index from an atomic counter, rank their
+// elements (warp multisplit), publish their per-digit counts, look back over
+// the preceding tiles' published counts for their global per-digit base and
+// scatter through shared memory.  Per pass: 16 B/element (+~6 B per 4096
+// elements of look-back status, L2-resident) instead of 20 B plus a device
+// scan of the 256 x blocks histogram.
+//
+// Look-back status word (u64): hi = epoch << 2 | flag (1 aggregate,
+// 2 inclusive prefix), lo = count.  The epoch changes every pass, so the
+// buffer is never cleared between passes.
+
+// lanes holding the same 8-bit digit as this lane (valid lanes only)
+__device__ __forceinline__ unsigned warp_peers8(uint32_t d, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    unsigned m;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+        "@!p not.b32 %0, %0;\n\t}"
+        : "=r"(m)
+        : "r"(d), "r"(1u << b));
+    peers &= m;
+  }
+  return peers;
+}
+
+constexpr int kHistThreads = 256;
+// global histograms of NPASS consecutive 8-bit digits (shift0, shift0+8, ...)
+// into ghist[pass][256] (zeroed by the caller).  aggmask bit p: digit p is
+// skewed (few distinct values) -> warp-aggregated counts.
+__global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __restrict__ keys,
+                                                             long long n, int shift0, int npass,
+                                                             unsigned aggmask,
+                                                             uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t s_h[4][256];
+  for (int q = threadIdx.x; q < 4 * 256; q += kHistThreads) (&s_h[0][0])[q] = 0;
+  __syncthreads();
+  const long long n4 = n >> 2;
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+  const long long stride = (long long)gridDim.x * kHistThreads;
+  // whole-warp trip count so the aggregated (ballot) path stays converged
+  const long long nround = (n4 + stride - 1) / stride;
+  for (long long it = 0; it < nround; ++it) {
+    const long long e = it * stride + (long long)blockIdx.x * kHistThreads + threadIdx.x;
+    const bool ok = e < n4;
+    const uint4 v = ok ? k4[e] : make_uint4(0, 0, 0, 0);
+    for (int p = 0; p < npass; ++p) {
+      const int sh = shift0 + 8 * p;
+      const uint32_t d0 = (v.x >> sh) & 255u, d1 = (v.y >> sh) & 255u;
+      const uint32_t d2 = (v.z >> sh) & 255u, d3 = (v.w >> sh) & 255u;
+      if ((aggmask >> p) & 1u) {
+        // run-aggregate the 4 keys, then across the warp
+        const bool same = ok && d0 == d1 && d0 == d2 && d0 == d3;
+        if (ok && !same) {
+          atomicAdd(&s_h[p][d0], 1u);
+          atomicAdd(&s_h[p][d1], 1u);
+          atomicAdd(&s_h[p][d2], 1u);
+          atomicAdd(&s_h[p][d3], 1u);
+        }
+        const unsigned peers = warp_peers8(d0, same);
+        if (same && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
+          atomicAdd(&s_h[p][d0], 4u * (uint32_t)__popc(peers));
+      } else if (ok) {
+        atomicAdd(&s_h[p][d0], 1u);
+        atomicAdd(&s_h[p][d1], 1u);
+        atomicAdd(&s_h[p][d2], 1u);
+        atomicAdd(&s_h[p][d3], 1u);
+      }
+    }
+  }
+  // tail (n % 4) in block 0
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const uint32_t k = keys[(n4 << 2) + threadIdx.x];
+    for (int p = 0; p < npass; ++p) atomicAdd(&s_h[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < npass * 256; q += kHistThreads) {
+    const uint32_t c = (&s_h[0][0])[q];
+    if (c) atomicAdd(&ghist[q], c);
+  }
+}
+
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// one stable pass on digit (key >> shift) & 255; ghist = this digit's global
+// histogram; look = [tiles][256] status words; ctr = tile counter (zeroed).
+template <int ITEMS>
+__global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
+    const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ look,
+    uint32_t* __restrict__ ctr, uint32_t epoch) {
+  constexpr int TILE = kSortThreads * ITEMS;
+  __shared__ uint32_t s_cnt[kSortWarps][256];  // counts -> block-local warp offsets
+  __shared__ uint32_t s_off[256];              // global base - block-local offset
+  __shared__ uint32_t s_k[TILE];
+  __shared__ uint32_t s_v[TILE];
+  __shared__ uint32_t s_ws[2][kSortWarps];
+  __shared__ uint32_t s_bid;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x == 0) s_bid = atomicAdd(ctr, 1u);
+  for (int q = threadIdx.x; q < kSortWarps * 256; q += kSortThreads) (&s_cnt[0][0])[q] = 0;
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const long long bbase = (long long)bid * TILE;
+  const long long wbase = bbase + (long long)w * (ITEMS * 32);
+  uint32_t kr[ITEMS], vr[ITEMS], dl[ITEMS];  // dl = digit | rank << 9
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const long long e = wbase + q * 32 + lane;
+    const bool ok = e < n;
+    kr[q] = ok ? keys[e] : 0u;
+    vr[q] = ok ? vals[e] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const bool ok = wbase + q * 32 + lane < n;
+    const uint32_t d = ok ? ((kr[q] >> shift) & 255u) : 256u;
+    const unsigned peers = warp_peers8(d, ok);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (ok && lane == leader) old = atomicAdd(&s_cnt[w][d], (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
+    dl[q] = d | ((old + __popc(peers & lt)) << 9);
+  }
+  __syncthreads();
+  const int d = threadIdx.x;  // kSortThreads == 256: one digit per thread
+  uint32_t acc = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww) {
+    const uint32_t c = s_cnt[ww][d];
+    s_cnt[ww][d] = acc;
+    acc += c;
+  }
+  // publish this tile's count of digit d as early as possible
+  unsigned long long* my = look + (size_t)bid * 256 + d;
+  const unsigned long long hiA = (unsigned long long)((epoch << 2) | 1u) << 32;
+  const unsigned long long hiP = (unsigned long long)((epoch << 2) | 2u) << 32;
+  st_status(my, (bid == 0 ? hiP : hiA) | acc);
+  // block-local digit offsets and global digit starts (two 256-wide scans)
+  const uint32_t gh = ghist[d];
+  uint32_t i1 = acc, i2 = gh;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y1 = __shfl_up_sync(0xffffffffu, i1, o);
+    const uint32_t y2 = __shfl_up_sync(0xffffffffu, i2, o);
+    if (lane >= o) { i1 += y1; i2 += y2; }
+  }
+  if (lane == 31) { s_ws[0][w] = i1; s_ws[1][w] = i2; }
+  // look back for the exclusive prefix of digit d over the preceding tiles
+  uint32_t excl = 0;
+  if (bid > 0) {
+    const unsigned long long* p = look + (size_t)(bid - 1) * 256 + d;
+    for (;;) {
+      unsigned long long s;
+      do {
+        s = ld_status(p);
+      } while ((uint32_t)(s >> 34) != epoch || ((s >> 32) & 3u) == 0u);
+      excl += (uint32_t)s;
+      if (((s >> 32) & 3u) == 2u) break;
+      p -= 256;
+    }
+    st_status(my, hiP | (excl + acc));
+  }
+  __syncthreads();
+  uint32_t p1 = 0, p2 = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww)
+    if (ww < w) { p1 += s_ws[0][ww]; p2 += s_ws[1][ww]; }
+  const uint32_t loff = p1 + i1 - acc;
+  s_off[d] = (p2 + i2 - gh) + excl - loff;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww) s_cnt[ww][d] += loff;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const uint32_t dq = dl[q] & 511u;
+    if (dq < 256) {
+      const uint32_t p = s_cnt[w][dq] + (dl[q] >> 9);
+      s_v[p] = vr[q];
+      s_k[p] = kr[q];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)min((long long)TILE, n - bbase);
+  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
+    const uint32_t k = s_k[p];
+    const uint32_t gp = s_off[(k >> shift) & 255u] + (uint32_t)p;
+    vals_out[gp] = s_v[p];
+    keys_out[gp] = k;
+  }
+}
+
 }  // namespace cr
