@@ -2,16 +2,17 @@
 // the CoherentRaster B200 path.  Unity build: includes every kernel header so
 // the __constant__ rig is shared without relocatable device code.
 //
-// Per-frame launch sequence (one stream, DESIGN.md §2):
-//   preprocess<DEG>           a4 (+a6 count)           HBM/ALU
-//   scan(cnt>0) -> compact    visible (i,k) records    HBM
-//   radix x4 (depth) + x1 (k) a7 depth presort          HBM
-//   scan(counts)              pair offsets, P          HBM
-//   emit                      a6 <tile, r> pairs        ALU
-//   radix x2..3 (tile)        a7 stable tile sort       HBM
-//   ranges                    a8                        HBM
-//   composite                 a9                        ALU/MUFU
-// Host<->device: two 4-byte reads (visible-record count, P) size the sorts.
+// Per-frame launch sequence (one stream, DESIGN.md §1):
+//   preprocess<DEG>             a4 per-(i,k) records + exact band pre-cull   HBM/ALU
+//   scan(vis) -> (key, r)       visible records, compressed presort keys     HBM
+//   onesweep x4 (k, depth)      a7 depth presort of the records              HBM/issue
+//   count + count_big           a6 cluster tile unions, list-position order  ALU
+//   scan(counts)                pair offsets, P                              HBM
+//   emit_flat + emit_big        a6 <tile, r> pairs in (k, depth, i) order    HBM
+//   hist + onesweep x2..3       a7 stable tile sort                          HBM/issue
+//   ranges                      a8                                           HBM
+//   composite                   a9                                           ALU/MUFU
+// Host<->device: two small reads (visible records + depth range, P) size the sorts.
 #include <cuda_runtime.h>
 #include <execinfo.h>
 #include <signal.h>
@@ -45,27 +46,15 @@ struct DevBuf {
 };
 
 struct Scan {  // functors for the generic device scan
-  struct OutIdx {  // compaction: write the index of every flagged element
-    uint32_t* o;
-    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
-      if (v) o[ex] = (uint32_t)i;
-    }
-  };
-  struct InCntPos {  // flag: record list[e] has >= 1 tile
-    const uint32_t* cnt;
-    const uint32_t* list;
-    __device__ uint32_t operator()(long long e) const { return cnt[list[e]] > 0u ? 1u : 0u; }
-  };
-  struct OutCompactList {  // presort key: (k << B) | (depth bits - dmin) when it fits 32 bits
-    const uint32_t* list;
+  struct OutCompactVis {  // visible record r -> presort (key, r), same key as OutCompactList
     const uint32_t* dkey;
     uint32_t* ko;
     uint32_t* vo;
     const uint32_t* drange;
     int kbits;
-    __device__ void operator()(long long e, uint32_t ex, uint32_t v) const {
+    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
       if (!v) return;
-      const uint32_t r = list[e];
+      const uint32_t r = (uint32_t)i;
       const uint32_t d = dkey[r], lo = drange[0], span = drange[1] - lo;
       const int B = span ? 32 - __clz(span) : 1;
       uint32_t key = d;
@@ -76,11 +65,6 @@ struct Scan {  // functors for the generic device scan
       ko[ex] = key;
       vo[ex] = r;
     }
-  };
-  struct InGather {
-    const uint32_t* cnt;
-    const uint32_t* idx;
-    __device__ uint32_t operator()(long long i) const { return cnt[idx[i]]; }
   };
   struct InArr {
     const uint32_t* a;
@@ -116,7 +100,7 @@ struct cr_ctx {
   std::vector<CamConstDev> ccon;
   float znear = 0.01f;
   // frame buffers
-  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, vlist, slots, elist, biglist;
+  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, slots, biglist;
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
   DevBuf bsum, hist, scalars, S, E, stage_out, frames;
@@ -281,7 +265,8 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
 // aggmask bit p: digit p is skewed (band mode), aggregate its histogram.
 constexpr int kOneItems = 16;
 cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uint32_t*& vB,
-                     long long n, int shift0, int npass, unsigned aggmask = 0) {
+                     long long n, int shift0, int npass, unsigned aggmask = 0,
+                     bool hist_ready = false) {
   if (n <= 0 || npass <= 0) return CR_OK;
   if (npass > 4) return fail(c, CR_ERR_CAPACITY, "radix_sort: npass %d > 4", npass);
   constexpr long long kTile = (long long)kSortThreads * kOneItems;
@@ -295,11 +280,17 @@ cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uin
   }
   uint32_t* gh = P_<uint32_t>(c->hist);
   uint32_t* ctr = gh + 4 * 256;
-  CR_CUDA(c, cudaMemsetAsync(gh, 0, (4 * 256 + 16) * 4, c->stream));
+  if (hist_ready) {  // histograms already in c->hist (k_bin): zero only the tile counters
+    CR_CUDA(c, cudaMemsetAsync(ctr, 0, 16 * 4, c->stream));
+  } else {
+    CR_CUDA(c, cudaMemsetAsync(gh, 0, (4 * 256 + 16) * 4, c->stream));
+  }
   const unsigned hgrid = (unsigned)std::max<long long>(
       1, std::min<long long>((n / 4 + kHistThreads - 1) / kHistThreads, 148 * 8));
-  k_radix_hist<<<hgrid, kHistThreads, 0, c->stream>>>(kA, n, shift0, npass, aggmask, gh);
-  CR_LAUNCHED(c);
+  if (!hist_ready) {
+    k_radix_hist<<<hgrid, kHistThreads, 0, c->stream>>>(kA, n, shift0, npass, aggmask, gh);
+    CR_LAUNCHED(c);
+  }
   for (int p = 0; p < npass; ++p) {
     if (++c->epoch >= (1u << 30)) {  // never in practice; keep the tags unambiguous
       CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
@@ -411,7 +402,7 @@ void cr_destroy(cr_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
-                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->vlist, &c->slots, &c->elist, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
+                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist, &c->look,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
@@ -664,7 +655,6 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->rec0, Rz * 32));  // AoS 32-byte records (rec1 unused)
   CR_TRY(ensure(c, c->geom, Rz * 32));
   CR_TRY(ensure(c, c->vis, Rz * 4));
-  CR_TRY(ensure(c, c->vlist, Rz * 4));
   CR_TRY(ensure(c, c->cnt, Rz * 4));
   CR_TRY(ensure(c, c->dkey, Rz * 4));
   CR_TRY(ensure(c, c->ka, Rz * 4));
@@ -673,12 +663,11 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->vb, Rz * 4));
   CR_TRY(ensure(c, c->offs, Rz * 4));
   CR_TRY(ensure(c, c->slots, Rz * 64));
-  CR_TRY(ensure(c, c->elist, Rz * 4));
   CR_TRY(ensure(c, c->biglist, Rz * 4));
   int G = 1;
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
-  uint32_t nvis = 0, nvis0 = 0;
+  uint32_t nvis = 0;
   uint32_t drange_h[2] = {0u, 0u};
   int kbits = 0;  // bits of the cluster id in the compressed presort key
   while ((1 << kbits) < K) ++kbits;
@@ -698,44 +687,16 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 #undef CR_PRE
     CR_LAUNCHED(c);
     CR_TRACE(c, "preprocess");
-    // visible (i,k) records, (k, i) order
-    CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->vis)}, Scan::OutIdx{P_<uint32_t>(c->vlist)}, R,
-                    sc + 4));
-    CR_TRY(read_u32(c, sc + 4, &nvis0));
-    CR_CUDA(c, cudaMemsetAsync(c->cnt.p, 0, (size_t)R * 4, str));
-    if (nvis0 > 0) {
-#define CR_COUNT(GG)                                                                          \
-  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->vlist), nvis0,               \
-                                                 P_<float4>(c->mean4), P_<float4>(c->geom),   \
-                                                 P_<uint32_t>(c->cnt), P_<uint4>(c->slots),   \
-                                                 P_<uint32_t>(c->biglist), sc + 6);           \
-  CR_LAUNCHED(c);                                                                             \
-  k_count_big<GG><<<bin_grid, kBinThreads, 0, str>>>(P_<uint32_t>(c->biglist), sc + 6,        \
-                                                     P_<float4>(c->mean4), P_<float4>(c->geom), \
-                                                     P_<uint32_t>(c->cnt))
-      switch (G) {
-        case 1: CR_COUNT(1); break;
-        case 2: CR_COUNT(2); break;
-        case 4: CR_COUNT(4); break;
-        case 8: CR_COUNT(8); break;
-        case 16: CR_COUNT(16); break;
-        default: CR_COUNT(32); break;
-      }
-#undef CR_COUNT
-      CR_LAUNCHED(c);
-      CR_TRACE(c, "count");
-      // records with >= 1 tile in the band -> (depth key, r)
-      CR_TRY(dev_scan(c, Scan::InCntPos{P_<uint32_t>(c->cnt), P_<uint32_t>(c->vlist)},
-                      Scan::OutCompactList{P_<uint32_t>(c->vlist), P_<uint32_t>(c->dkey),
-                                           P_<uint32_t>(c->ka), P_<uint32_t>(c->va), sc + 16,
-                                           kbits},
-                      nvis0, sc + 0));
-      uint32_t hw[18];
-      CR_TRY(read_words(c, sc, hw, 18));  // nvis and the depth-bit range in one read
-      nvis = hw[0];
-      drange_h[0] = hw[16];
-      drange_h[1] = hw[17];
-    }
+    // visible (i,k) records straight to presort (key, r) pairs, (k, i) order
+    CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->vis)},
+                    Scan::OutCompactVis{P_<uint32_t>(c->dkey), P_<uint32_t>(c->ka),
+                                        P_<uint32_t>(c->va), sc + 16, kbits},
+                    R, sc + 0));
+    uint32_t hw[18];
+    CR_TRY(read_words(c, sc, hw, 18));  // nvis and the depth-bit range in one read
+    nvis = hw[0];
+    drange_h[0] = hw[16];
+    drange_h[1] = hw[17];
     CR_TRACE(c, "compaction");
   }
   CR_CUDA(c, cudaEventRecord(c->ev[1], str));
@@ -762,13 +723,36 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 
   // ---- a6 offsets + emit
   uint32_t P = 0;
+  int tbits = 1;
+  while ((1LL << tbits) < (long long)TX * TY) ++tbits;
+  const int tpass = (tbits + 7) / 8;
   if (nvis > 0) {
-    CR_TRY(dev_scan(c, Scan::InGather{P_<uint32_t>(c->cnt), rec_sorted},
-                    Scan::OutStore{P_<uint32_t>(c->offs)}, nvis, sc + 1));
-    CR_TRY(read_u32(c, sc + 1, &P));
-    uint32_t ovf = 0;
-    CR_TRY(read_u32(c, sc + 3, &ovf));
-    if (ovf) return fail(c, CR_ERR_CAPACITY, "pair count exceeds 2^32-1");
+    // count in (k, depth, i) order: position-indexed counts and union slots
+#define CR_COUNTS(GG)                                                                         \
+  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(                                       \
+      rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),      \
+      P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                                 \
+  CR_LAUNCHED(c);                                                                             \
+  k_count_big<GG><<<bin_grid, kBinThreads, 0, str>>>(                                   \
+      P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
+      P_<uint32_t>(c->cnt))
+    switch (G) {
+      case 1: CR_COUNTS(1); break;
+      case 2: CR_COUNTS(2); break;
+      case 4: CR_COUNTS(4); break;
+      case 8: CR_COUNTS(8); break;
+      case 16: CR_COUNTS(16); break;
+      default: CR_COUNTS(32); break;
+    }
+#undef CR_COUNTS
+    CR_LAUNCHED(c);
+    CR_TRACE(c, "count");
+    CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->cnt)}, Scan::OutStore{P_<uint32_t>(c->offs)},
+                    nvis, sc + 1));
+    uint32_t hw[4];
+    CR_TRY(read_words(c, sc, hw, 4));
+    P = hw[1];
+    if (hw[3]) return fail(c, CR_ERR_CAPACITY, "pair count exceeds 2^32-1");
   }
   const size_t Pz = std::max<size_t>(P, 1);
   CR_TRY(ensure(c, c->pta, Pz * 4));
@@ -778,39 +762,34 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   uint32_t *tA = P_<uint32_t>(c->pta), *pA = P_<uint32_t>(c->pva);
   uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
   if (P > 0) {
-    uint32_t* n_el = sc + 5;
-    CR_CUDA(c, cudaMemsetAsync(n_el, 0, 4, str));
-    k_emit_slots<<<grid_for(nvis, 256), 256, 0, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis,
-                                                       P_<uint4>(c->slots), tA, pA,
-                                                       P_<uint32_t>(c->elist), n_el);
+    k_emit_flat<<<(unsigned)std::min<long long>((nvis + 255) / 256, 148 * 16), 256, 0, str>>>(
+        rec_sorted, P_<uint32_t>(c->offs), nvis, P, P_<uint4>(c->slots), tA, pA);
     CR_LAUNCHED(c);
-#define CR_EMITG(GG)                                                                        \
+#define CR_EMITB(GG)                                                                        \
   k_emit_big<GG><<<bin_grid, kBinThreads, 0, str>>>(                                        \
-      rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->elist), n_el, P_<float4>(c->mean4), \
+      rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->biglist), sc + 6, P_<float4>(c->mean4), \
       P_<float4>(c->geom), tA, pA)
     switch (G) {
-      case 1: CR_EMITG(1); break;
-      case 2: CR_EMITG(2); break;
-      case 4: CR_EMITG(4); break;
-      case 8: CR_EMITG(8); break;
-      case 16: CR_EMITG(16); break;
-      default: CR_EMITG(32); break;
+      case 1: CR_EMITB(1); break;
+      case 2: CR_EMITB(2); break;
+      case 4: CR_EMITB(4); break;
+      case 8: CR_EMITB(8); break;
+      case 16: CR_EMITB(16); break;
+      default: CR_EMITB(32); break;
     }
-#undef CR_EMITG
+#undef CR_EMITB
     CR_LAUNCHED(c);
   }
   CR_TRACE(c, "offsets+emit");
   CR_CUDA(c, cudaEventRecord(c->ev[3], str));
 
   // ---- a7 stable tile sort + a8 ranges
-  int tbits = 1;
-  while ((1LL << tbits) < (long long)TX * TY) ++tbits;
   {
     // digits that span only the band's few tile rows: aggregate their histograms
     unsigned agg = 0;
     for (int sh = 8, q = 1; sh < tbits; sh += 8, ++q)
       if (((long long)(row1 - row0) * TX >> sh) < 64) agg |= 1u << q;
-    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, (tbits + 7) / 8, agg));
+    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, tpass, agg));
   }
   const size_t nSE = (size_t)TX * TY * K;
   CR_TRY(ensure(c, c->S, nSE * 4));
@@ -895,7 +874,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     st->culled_opacity = (int64_t)cnts[2];
     st->evals = (int64_t)cnts[3];
     uint32_t nfb = 0;
-    CR_CUDA(c, cudaMemcpy(&nfb, sc + 5, 4, cudaMemcpyDeviceToHost));
+    CR_CUDA(c, cudaMemcpy(&nfb, sc + 6, 4, cudaMemcpyDeviceToHost));
     st->emit_fallback = (int32_t)nfb;
     st->num_clusters = K;
     st->bit_k = bitK;
@@ -988,6 +967,16 @@ cr_status cr_get_counts(cr_ctx* c, uint32_t* dst, size_t* n) {
   if (!c) return CR_ERR_INVALID_ARG;
   if (!c->has_frame) return fail(c, CR_ERR_NOT_READY, "no frame rendered");
   cudaSetDevice(c->device);
+  if (dst) {  // |T_{i,k}| recovered from the emitted pairs (payload r); cnt is per list position
+    const size_t R = (size_t)c->K * c->M;
+    CR_TRY(ensure(c, c->cnt, std::max<size_t>(R, 1) * 4));
+    CR_CUDA(c, cudaMemsetAsync(c->cnt.p, 0, R * 4, c->stream));
+    if (c->P > 0) {
+      k_pair_counts<<<grid_for(c->P, 256), 256, 0, c->stream>>>(c->final_v, c->P,
+                                                               P_<uint32_t>(c->cnt));
+      CR_LAUNCHED(c);
+    }
+  }
   return copy_out(c, dst, c->cnt.p, (size_t)c->K * c->M, 4, n);
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 
 #include "cr_device.cuh"
+#include "cr_sort.cuh"
 
 namespace cr {
 
@@ -234,6 +235,22 @@ __device__ __forceinline__ unsigned long long gor64(unsigned long long v) {
   return v;
 }
 
+// Position of the n-th (0-based) set bit of x (n < popc(x)): popcount
+// bisection over halves, bytes, nibbles, pairs — branch-free, ~20 ALU ops
+// (the __fns intrinsic is a much longer software sequence).
+__device__ __forceinline__ int nth_set_bit(unsigned x, int n) {
+  int pos = 0;
+  int c = __popc(x & 0xFFFFu);
+  if (n >= c) { n -= c; x >>= 16; pos += 16; }
+  c = __popc(x & 0xFFu);
+  if (n >= c) { n -= c; x >>= 8; pos += 8; }
+  c = __popc(x & 0xFu);
+  if (n >= c) { n -= c; x >>= 4; pos += 4; }
+  c = __popc(x & 0x3u);
+  if (n >= c) { n -= c; x >>= 2; pos += 2; }
+  return pos + ((n >= (int)(x & 1u)) ? 1 : 0);
+}
+
 // ===========================================================================
 // O8 — cluster tile union (Alg.2 GenerateKeys) restricted to the
 // band rows, computed by a GROUP of G lanes: lane v of the group owns view
@@ -253,7 +270,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
                                 float muy, float muz, const EllRec& el, int it0, int istep,
                                 uint32_t* __restrict__ row_cnt, const uint32_t* __restrict__ row_off,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
-                                uint32_t payload) {
+                                uint32_t payload, uint32_t cap = 0xFFFFFFFFu) {
   // MODE 0: count the group's rows; MODE 3: also store per-row counts in
   // row_cnt[it]; MODE 2: write the tiles of row it at row_off[it] + rank.
   // The group handles union rows it = it0, it0 + istep, ...
@@ -316,9 +333,11 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
           const unsigned lo32 = (unsigned)mask, hi32 = (unsigned)(mask >> 32);
           const int pl = __popc(lo32);
           for (int q = (int)(threadIdx.x & (G - 1)); q < pc; q += G) {
-            const int bit = q < pl ? (int)__fns(lo32, 0, q + 1) : 32 + (int)__fns(hi32, 0, q - pl + 1);
-            out_t[rowpos + q] = rowbase + (uint32_t)(wlo + bit);
-            out_v[rowpos + q] = payload;
+            const int bit = q < pl ? nth_set_bit(lo32, q) : 32 + nth_set_bit(hi32, q - pl);
+            if (rowpos + q < cap) {  // capacity guard (the host re-runs with the exact size)
+              out_t[rowpos + q] = rowbase + (uint32_t)(wlo + bit);
+              out_v[rowpos + q] = payload;
+            }
           }
           rowpos += (uint32_t)pc;
         }
@@ -356,24 +375,28 @@ __device__ __forceinline__ bool may_touch_band(int k, float mx, float my, float 
   const float S = fabsf(mx) + fabsf(my) + fabsf(mz);
   const float ylo = 16.0f * (float)c_fp.row0 - 16.0f, yhi = 16.0f * (float)c_fp.row1 + 16.0f;
   const float xlo = -16.0f, xhi = 16.0f * (float)c_fp.TX + 16.0f;
-  for (int j = j0; j < j1; ++j) {
+  bool hit = false;
+  for (int j = j0; j < j1; ++j) {  // j is warp-uniform (one k per launch-wide loop step)
     const CamDev& c = c_cams[j];
     const float px = fmaf(c.R[0], mx, fmaf(c.R[1], my, fmaf(c.R[2], mz, c.t[0])));
     const float py = fmaf(c.R[3], mx, fmaf(c.R[4], my, fmaf(c.R[5], mz, c.t[1])));
     const float pz = fmaf(c.R[6], mx, fmaf(c.R[7], my, fmaf(c.R[8], mz, c.t[2])));
     const float err = 4e-6f * (S + fabsf(c.t[0]) + fabsf(c.t[1]) + fabsf(c.t[2]) + 1.0f);
     if (pz + err < c_fp.znear) continue;        // certainly invisible from view j
-    if (pz < 2.0f * c_fp.znear + err) return true;  // too close to call
+    if (pz < 2.0f * c_fp.znear + err) {         // too close to call
+      hit = true;
+      continue;
+    }
     const float iz = __fdividef(1.0f, pz);  // approximate: covered by the padding
     const float u = px * iz, v = py * iz;
     const float ex = c.fx * u + c.cx, ey = c.fy * v + c.cy;
     const float mgx = c.fx * err * iz * (1.0f + fabsf(u)) * 2.0f + 1e-5f * fabsf(ex) + 1.0f;
     const float mgy = c.fy * err * iz * (1.0f + fabsf(v)) * 2.0f + 1e-5f * fabsf(ey) + 1.0f;
-    if (ey + eyw + mgy >= ylo && ey - eyw - mgy <= yhi && ex + exw + mgx >= xlo &&
-        ex - exw - mgx <= xhi)
-      return true;
+    const bool in = ey + eyw + mgy >= ylo && ey - eyw - mgy <= yhi && ex + exw + mgx >= xlo &&
+                    ex - exw - mgx <= xhi;
+    hit |= in;  // no early exit: the warp stays converged over the cluster's views
   }
-  return false;
+  return hit;
 }
 
 template <int DEG>
@@ -510,6 +533,9 @@ struct BinWarpSmem {
   unsigned long long mask[32][kSlotRows];     // per group, per row
 };
 
+// recs is the depth-sorted record list and every output is indexed by the list
+// position g (cnt[g], slot g, big list of positions), so the offsets scan and
+// the emission read them sequentially.
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
                                                        uint32_t n,
@@ -639,6 +665,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
     // ---- finalize fast records; general path for the rest
     const bool slow = active && nrows > 0 && (!fast || s_flag[w][gi] != 0);
     uint32_t c = 0;
+    const unsigned long long o = g;  // output index: list position
     if (active && fast && !slow && lead) {
       unsigned long long mk[kSlotRows];
 #pragma unroll
@@ -646,61 +673,88 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
         mk[t] = s_mask[w][gi][t];
         c += (uint32_t)__popcll(mk[t]);
       }
-      uint4* sl = slots + 4ull * r;
+      uint4* sl = slots + 4ull * o;
       sl[0] = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
       sl[1] = make_uint4((uint32_t)mk[0], (uint32_t)(mk[0] >> 32), (uint32_t)mk[1], (uint32_t)(mk[1] >> 32));
       sl[2] = make_uint4((uint32_t)mk[2], (uint32_t)(mk[2] >> 32), (uint32_t)mk[3], (uint32_t)(mk[3] >> 32));
       sl[3] = make_uint4((uint32_t)mk[4], (uint32_t)(mk[4] >> 32), (uint32_t)mk[5], (uint32_t)(mk[5] >> 32));
     }
     if (slow && lead) {  // footprint beyond the fast path: k_count_big
-      slots[4ull * r] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
-      big[atomicAdd(n_big, 1u)] = r;
+      slots[4ull * o] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
+      big[atomicAdd(n_big, 1u)] = (uint32_t)o;
     }
-    if (active && lead) cnt[r] = c;
+    if (active && lead) cnt[o] = c;
     __syncwarp();
   }
 }
 
 // ===========================================================================
-// a6 emit, fast path — one thread per depth-sorted record e decodes the union
-// slot written by k_count and writes <tile, r> at offs[e].  Records flagged
-// in their slot are appended to `elist` for k_emit_big.
+// a6 emit, fast path over the depth-sorted, position-indexed slots (k_count
+// SORTED): each warp takes 32 consecutive records (lane = record), whose pairs
+// form one contiguous output range.  Each lane decodes its record's union
+// slot bit by bit into a shared-memory window of kEmitWin pairs (rows
+// ascending, tiles ascending), then the warp copies the window out with
+// coalesced stores.  Window positions of records flagged overflow are left
+// to k_emit_big, which runs afterwards and overwrites them.  Grid-stride over
+// record blocks.
 // ===========================================================================
-__global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__ rec_sorted,
-                                                    const uint32_t* __restrict__ offs, uint32_t n,
-                                                    const uint4* __restrict__ slots,
-                                                    uint32_t* __restrict__ out_t,
-                                                    uint32_t* __restrict__ out_v,
-                                                    uint32_t* __restrict__ elist,
-                                                    uint32_t* __restrict__ n_elist) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const uint32_t r = rec_sorted[e];
-  const uint4* sl = slots + 4ull * r;
-  const uint4 h = sl[0];
-  if (h.x & kSlotOverflow) {
-    elist[atomicAdd(n_elist, 1u)] = e;
-    return;
-  }
-  const uint32_t row0 = h.x & 0xFFFF, nrows = (h.x >> 16) & 0xFF;
-  const uint32_t lo = h.y;
+constexpr int kEmitWin = 256;
+__global__ void __launch_bounds__(256) k_emit_flat(const uint32_t* __restrict__ rec_sorted,
+                                                   const uint32_t* __restrict__ offs, uint32_t n,
+                                                   uint32_t P, const uint4* __restrict__ slots,
+                                                   uint32_t* __restrict__ out_t,
+                                                   uint32_t* __restrict__ out_v) {
+  __shared__ uint32_t s_t[8][kEmitWin];
+  __shared__ uint32_t s_v[8][kEmitWin];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t TX = (uint32_t)c_fp.TX;
-  uint32_t o = offs[e];
-  for (uint32_t q = 0; q < nrows; q += 2) {
-    const uint4 mk = sl[1 + (q >> 1)];
-    unsigned long long m2[2] = {(unsigned long long)mk.x | ((unsigned long long)mk.y << 32),
-                                (unsigned long long)mk.z | ((unsigned long long)mk.w << 32)};
+  const uint32_t nblk = (n + 31) / 32;
+  for (uint32_t b = blockIdx.x * 8u + (uint32_t)w; b < nblk; b += gridDim.x * 8u) {
+    const uint32_t e = b * 32u + (uint32_t)lane;
+    const bool ok = e < n;
+    const uint32_t o = ok ? offs[e] : P;
+    const uint32_t f0 = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t f1 = b * 32u + 32u < n ? offs[b * 32u + 32u] : P;
+    uint32_t o1 = __shfl_down_sync(0xffffffffu, o, 1);  // next record's offset
+    if (lane == 31) o1 = f1;
+    const uint32_t r = ok ? rec_sorted[e] : 0u;
+    // the slot of a record without tiles in the band is never written: test the count first
+    const uint4 h = (ok && o1 > o) ? slots[4ull * e] : make_uint4(kSlotOverflow, 0u, 0u, 0u);
+    const bool dec = !(h.x & kSlotOverflow);  // fast record with >= 1 tile
+    const uint32_t nrows = (h.x >> 16) & 0xFFu;
+    const uint32_t lo = o - f0, hi = o1 - f0;  // local pair range
+    for (uint32_t wb = 0; wb < f1 - f0; wb += kEmitWin) {  // warp-uniform
+      if (dec && hi > wb && lo < wb + kEmitWin) {
+        uint32_t q = lo;
+        for (uint32_t t = 0; t < nrows && q < wb + kEmitWin; t += 2) {
+          const uint4 mk = slots[4ull * e + 1 + (t >> 1)];
+          unsigned long long m2[2] = {(unsigned long long)mk.x | ((unsigned long long)mk.y << 32),
+                                      (unsigned long long)mk.z | ((unsigned long long)mk.w << 32)};
 #pragma unroll
-    for (int qq = 0; qq < 2; ++qq) {
-      unsigned long long m = (q + qq < nrows) ? m2[qq] : 0ull;
-      const uint32_t base = (row0 + q + qq) * TX + lo;
-      while (m) {
-        const int bit = __ffsll((long long)m) - 1;
-        m &= m - 1;
-        out_t[o] = base + (uint32_t)bit;
-        out_v[o] = r;
-        ++o;
+          for (int tt = 0; tt < 2; ++tt) {
+            unsigned long long m = (t + tt < nrows) ? m2[tt] : 0ull;
+            const uint32_t pc = (uint32_t)__popcll(m);
+            if (q + pc <= wb) { q += pc; continue; }  // row entirely before the window
+            const uint32_t rowbase = ((h.x & 0xFFFFu) + t + tt) * TX + h.y;
+            while (m && q < wb + kEmitWin) {
+              const int bit = __ffsll((long long)m) - 1;
+              m &= m - 1;
+              if (q >= wb) {
+                s_t[w][q - wb] = rowbase + (uint32_t)bit;
+                s_v[w][q - wb] = r;
+              }
+              ++q;
+            }
+          }
+        }
       }
+      __syncwarp();
+      const uint32_t nw = min((uint32_t)kEmitWin, f1 - f0 - wb);
+      for (uint32_t i = (uint32_t)lane; i < nw; i += 32u) {
+        out_t[f0 + wb + i] = s_t[w][i];
+        out_v[f0 + wb + i] = s_v[w][i];
+      }
+      __syncwarp();
     }
   }
 }
@@ -712,6 +766,7 @@ __global__ void __launch_bounds__(256) k_emit_slots(const uint32_t* __restrict__
 // ===========================================================================
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __restrict__ big,
+                                                           const uint32_t* __restrict__ recs,
                                                            const uint32_t* __restrict__ n_ptr,
                                                            const float4* __restrict__ mean4,
                                                            const float4* __restrict__ geom,
@@ -724,18 +779,20 @@ __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __res
   const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
   const uint32_t nwarps = gridDim.x * kBinWarps;
   for (uint32_t g = (blockIdx.x * kBinThreads + threadIdx.x) / 32; g < n; g += nwarps) {
-    const uint32_t r = big[g];
+    const uint32_t o = big[g];
+    const uint32_t r = recs[o];
     const int k = (int)fdiv(r, c_fp.divM);
     const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
     const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
     const uint32_t c = group_union<0, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr,
                                          nullptr, nullptr, nullptr, 0);
     const uint32_t tot = __reduce_add_sync(0xffffffffu, v == 0 ? c : 0u);
-    if (lane == 0) cnt[r] = tot;
+    if (lane == 0) cnt[o] = tot;
   }
 }
 
 constexpr int kMaxRows = 288;  // >= TY for 8K (270 tile rows)
+constexpr int kMaxRowsBin = kMaxRows;
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
@@ -780,6 +837,14 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
                       r);
     __syncwarp();
   }
+}
+
+// Introspection (cr_get_counts): per-(i,k) tile counts |T_{i,k}| recovered from
+// the emitted pairs (each pair carries its record r).
+__global__ void k_pair_counts(const uint32_t* __restrict__ val, uint32_t P,
+                              uint32_t* __restrict__ cnt) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < P) atomicAdd(&cnt[val[e]], 1u);
 }
 
 // ===========================================================================

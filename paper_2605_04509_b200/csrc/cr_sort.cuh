@@ -370,6 +370,8 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
 
 // one stable pass on digit (key >> shift) & 255; ghist = this digit's global
 // histogram; look = [tiles][256] status words; ctr = tile counter (zeroed).
+// Ranks by 8-ballot multisplit peers (measured faster than match.any.sync on
+// B200: 4.37 vs 4.88 ms for the frame's 6 passes; 16 items/thread beat 12).
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
