@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=None,
                     help="oracle sample: tile rows (default 12 for cpu_baseline, 4 per --impl reference step)")
     ap.add_argument("--ablation", action="store_true", help="also time reuse/remap variants (stderr)")
+    ap.add_argument("--refine", type=int, default=2,
+                    help="band-split refinement rounds from measured band costs (N>1, balanced)")
     ap.add_argument("--bands", default="balanced", choices=["balanced", "equal"],
                     help="row-band split for N>1: equal-cost (calibration frame) or equal rows")
     args = ap.parse_args()
@@ -258,7 +260,23 @@ def main():
         # calibration frame (untimed): per-row pair counts -> equal-cost bands
         r.render(cfg.cluster_size)
         torch.cuda.synchronize()
-        bands = balanced_bands(row_pair_weights(r, cfg.cluster_size) + 2.0e5, world)
+        wrow = row_pair_weights(r, cfg.cluster_size) + 2.0e5
+        bands = balanced_bands(wrow, world)
+        # refine with MEASURED band costs (untimed): each rank renders its band,
+        # the variable time (total minus the replicated preprocess) is gathered
+        # and the per-row model rescaled band by band (multigpu.refine_bands)
+        from paper_2605_04509_b200.multigpu import refine_bands
+        cdev = dev if backend == "nccl" else torch.device("cpu")
+        for _ in range(args.refine):
+            cost = []
+            for _ in range(3):
+                r.render(cfg.cluster_size, rows=bands[rank], stats=True)
+                st_ = r.last_stats
+                cost.append(st_["ms_total"] - st_["ms_preprocess"])
+            mine = torch.tensor([min(cost)], dtype=torch.float64, device=cdev)
+            allc = torch.empty(world, dtype=torch.float64, device=cdev)
+            dist.all_gather_into_tensor(allc, mine)
+            bands, wrow = refine_bands(wrow, bands, allc.cpu().tolist(), world)
     bgt = BandGather(cfg.H, cfg.W, TY, world, rank, dev, bands=bands)
     rows = bgt.rows
     band_out = bgt.out

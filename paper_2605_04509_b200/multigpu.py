@@ -42,6 +42,27 @@ def balanced_bands(weights, world: int):
     return [(cuts[q], cuts[q + 1]) for q in range(world)]
 
 
+def refine_bands(weights, bands, costs, world: int):
+    """One refinement step of the band split from MEASURED per-band costs.
+
+    weights[ty]: the current per-row cost model (e.g. calibration pair counts);
+    bands: the split that was measured; costs[b]: band b's measured variable
+    time (total minus the replicated per-rank part).  Every row of band b is
+    rescaled by costs[b] / sum(weights in b), which keeps the within-band shape
+    of the model and corrects its scale where it mispredicts (e.g. rows of
+    background splats that are cheap to bin but slow to composite); the new
+    split balances the corrected weights.  Returns (new_bands, new_weights)."""
+    import numpy as np
+    w = np.asarray(weights, np.float64).copy()
+    for (r0, r1), c in zip(bands, costs):
+        tot = w[r0:r1].sum()
+        if tot > 0:
+            w[r0:r1] *= max(float(c), 0.0) / tot
+        else:
+            w[r0:r1] = max(float(c), 0.0) / max(1, r1 - r0)
+    return balanced_bands(w, world), w
+
+
 def _pix(H, r0, r1):
     return r0 * 16, min(H, r1 * 16)
 

@@ -39,6 +39,31 @@ def test_balanced_bands():
     assert mg.balanced_bands(np.ones(8), 8) == [(q, q + 1) for q in range(8)]
 
 
+def test_refine_bands_converges_to_true_cost():
+    # the model (uniform pairs) mispredicts a true per-row cost; refining with
+    # measured band costs must approach the true balanced split
+    TY, world = 135, 8
+    rng = np.random.default_rng(1)
+    true = 1.0 + 4.0 * np.exp(-((np.arange(TY) - 60) / 12.0) ** 2) + rng.uniform(0, 0.2, TY)
+    model = np.ones(TY)
+    bands = mg.balanced_bands(model, world)
+    worst0 = max(true[a:b].sum() for a, b in bands)
+    w = model
+    for _ in range(4):
+        costs = [true[a:b].sum() for a, b in bands]
+        bands, w = mg.refine_bands(w, bands, costs, world)
+        assert bands[0][0] == 0 and bands[-1][1] == TY
+        assert all(bands[q][1] == bands[q + 1][0] and bands[q][1] > bands[q][0] for q in range(world - 1))
+    worst = max(true[a:b].sum() for a, b in bands)
+    ideal = true.sum() / world
+    assert worst < worst0
+    assert worst <= ideal + 2 * true.max()
+    # exact model: refinement keeps the balanced split
+    b0 = mg.balanced_bands(true, world)
+    b1, _ = mg.refine_bands(true, b0, [true[a:b].sum() for a, b in b0], world)
+    assert b1 == b0
+
+
 def test_pose_split_covers_all():
     got = sorted(sum((mg.pose_split(256, 8, r) for r in range(8)), []))
     assert got == list(range(256)) and len(mg.pose_split(256, 8, 3)) == 32

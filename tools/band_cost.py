@@ -13,10 +13,22 @@ r.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset, c.view_cone
 r.set_camera_rig(c.make_rig())
 worst = 0
 bands = None
-if mode == "balanced":
+if mode in ("balanced", "refined"):
     r.render(c.cluster_size)
     torch.cuda.synchronize()
-    bands = balanced_bands(row_pair_weights(r, c.cluster_size) + 2.0e5, R)
+    wrow = row_pair_weights(r, c.cluster_size) + 2.0e5
+    bands = balanced_bands(wrow, R)
+    if mode == "refined":  # the bench's measured-cost refinement, simulated on one GPU
+        from paper_2605_04509_b200.multigpu import refine_bands
+        for _ in range(2):
+            costs = []
+            for q in range(R):
+                cs = []
+                for _ in range(3):
+                    r.render(c.cluster_size, rows=bands[q], stats=True)
+                    cs.append(r.last_stats["ms_total"] - r.last_stats["ms_preprocess"])
+                costs.append(min(cs))
+            bands, wrow = refine_bands(wrow, bands, costs, R)
 for q in range(R):
     rows = bands[q] if bands else band_rows(r.TY, R, q)
     for _ in range(2):
