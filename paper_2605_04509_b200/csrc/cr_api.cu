@@ -103,8 +103,10 @@ struct cr_ctx {
   DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, slots, biglist;
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
-  DevBuf bsum, hist, scalars, S, E, stage_out, frames;
+  DevBuf hist, scalars, S, E, stage_out, frames;
   DevBuf look;                     // onesweep look-back status words
+  DevBuf slook;                    // single-pass scan look-back status words + ticket
+  uint32_t sepoch = 0;
   uint32_t epoch = 0;              // look-back tag of the last radix pass
   DevBuf tmp;                      // upload staging
   uint32_t* h_pinned = nullptr;    // small pinned readback
@@ -214,14 +216,22 @@ cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
     return CR_OK;
   }
   const long long nb = (n + kScanTile - 1) / kScanTile;
-  CR_TRY(ensure(c, c->bsum, (size_t)nb * 4));
-  uint32_t* bs = P_<uint32_t>(c->bsum);
-  k_scan_reduce<In><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, n, bs);
-  CR_LAUNCHED(c);
+  const size_t lbytes = (size_t)nb * 8 + 64;  // the ticket counter + status words
+  if (lbytes > c->slook.bytes || !c->slook.p) {
+    CR_TRY(ensure(c, c->slook, lbytes));
+    CR_CUDA(c, cudaMemsetAsync(c->slook.p, 0, c->slook.bytes, c->stream));
+    c->sepoch = 0;
+  }
+  if (++c->sepoch >= (1u << 30)) {
+    CR_CUDA(c, cudaMemsetAsync(c->slook.p, 0, c->slook.bytes, c->stream));
+    c->sepoch = 1;
+  }
+  uint32_t* ticket = P_<uint32_t>(c->slook);  // first 64 bytes: ticket; then status words
+  unsigned long long* look = (unsigned long long*)((char*)c->slook.p + 64);
+  CR_CUDA(c, cudaMemsetAsync(ticket, 0, 4, c->stream));
   int* ovf = P_<int>(c->scalars) + 3;
-  k_scan_bsums<<<1, 1024, 0, c->stream>>>(bs, (int)nb, d_total, ovf);
-  CR_LAUNCHED(c);
-  k_scan_down<In, Out><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, out, n, bs);
+  k_scan_onepass<In, Out><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, out, n, look, ticket,
+                                                                         c->sepoch, d_total, ovf);
   CR_LAUNCHED(c);
   return CR_OK;
 }
@@ -403,7 +413,7 @@ void cr_destroy(cr_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
                    &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
-                   &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->bsum, &c->hist, &c->look,
+                   &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->hist, &c->look, &c->slook,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)

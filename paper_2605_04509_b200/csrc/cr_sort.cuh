@@ -1,11 +1,12 @@
-// cr_sort.cuh — device-wide exclusive scan and a CUB-free, stable LSD radix
-// sort (8-bit digits) of (u32 key, u32 value) pairs.  Used for
-//   * visible-record compaction (scan of cnt > 0),
-//   * the depth presort of records by (k, depth) (4 depth passes + 1 k pass),
+// cr_sort.cuh — device-wide single-pass exclusive scan and a CUB-free,
+// stable LSD radix sort (8-bit digits, onesweep) of (u32 key, u32 value)
+// pairs.  Used for
+//   * visible-record compaction straight to presort keys (scan of vis),
+//   * the depth presort of records by (k, depth) (compressed keys, <= 4 passes),
 //   * the pair offsets (scan of per-record tile counts),
 //   * the final stable tile sort of pairs (2 passes at 4K, 3 at 8K).
-// Memory-bound: per pass the upsweep reads the digit source (4 B) and the
-// downsweep reads key+value and writes key+value (16 B) -> 20 B/element.
+// Per onesweep pass: read key+value, write key+value (16 B/element) plus one
+// digit histogram pass per sort.
 #pragma once
 #include "cr_device.cuh"
 
@@ -46,57 +47,35 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& e
   return total;
 }
 
-// Phase 1: per-block sums of in(i).
-template <class In>
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(In in, long long n,
-                                                              uint32_t* __restrict__ bsum) {
-  __shared__ uint32_t s_warp[33];
-  const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
-  uint32_t v = 0;
-#pragma unroll
-  for (int q = 0; q < kScanItems; ++q)
-    if (base + q < n) v += in(base + q);
-  uint32_t ex;
-  const uint32_t tot = block_exclusive_scan<kScanThreads>(v, ex, s_warp);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+// Single-pass exclusive scan (decoupled look-back): CTA tiles in the order of
+// an atomic ticket; each publishes its aggregate, looks back over the
+// predecessors' status words for its exclusive prefix, publishes the
+// inclusive prefix and writes out(i, prefix, value).  One read of in, one
+// write of out (the 3-kernel scan reads in twice).  Status word (u64): hi =
+// epoch << 2 | flag (1 aggregate, 2 inclusive), lo = count; the epoch changes
+// every launch, so the buffer is never cleared.  *total = the sum; a sum
+// beyond 2^32-1 sets *overflow.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Phase 2: exclusive scan of the block sums in place (one block); total out.
-// Overflow beyond 2^32-1 sets *overflow.
-__global__ void __launch_bounds__(1024) k_scan_bsums(uint32_t* __restrict__ bsum, int nb,
-                                                     uint32_t* __restrict__ total,
-                                                     int* __restrict__ overflow) {
-  __shared__ uint32_t s_warp[33];
-  __shared__ unsigned long long s_big;
-  const int per = (nb + 1023) / 1024;
-  const int b0 = threadIdx.x * per;
-  unsigned long long v = 0;
-  for (int q = 0; q < per; ++q)
-    if (b0 + q < nb) v += bsum[b0 + q];
-  if (threadIdx.x == 0) s_big = 0;
-  __syncthreads();
-  atomicAdd(&s_big, v);
-  uint32_t ex;
-  block_exclusive_scan<1024>((uint32_t)v, ex, s_warp);
-  uint32_t run = ex;
-  for (int q = 0; q < per; ++q)
-    if (b0 + q < nb) {
-      const uint32_t x = bsum[b0 + q];
-      bsum[b0 + q] = run;
-      run += x;
-    }
-  if (threadIdx.x == 0) {
-    *total = (uint32_t)s_big;
-    if (s_big > 0xFFFFFFFFull && overflow) *overflow = 1;
-  }
-}
-
-// Phase 3: out(i, exclusive prefix, value).
 template <class In, class Out>
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(In in, Out out, long long n,
-                                                            const uint32_t* __restrict__ bsum) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
+    In in, Out out, long long n, unsigned long long* __restrict__ look,
+    uint32_t* __restrict__ ticket, uint32_t epoch, uint32_t* __restrict__ total,
+    int* __restrict__ overflow) {
   __shared__ uint32_t s_warp[33];
-  const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
+  __shared__ uint32_t s_bid, s_pre;
+  if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const long long nb = (n + kScanTile - 1) / kScanTile;
+  const long long base = (long long)bid * kScanTile + (long long)threadIdx.x * kScanItems;
   uint32_t vals[kScanItems], v = 0;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) {
@@ -104,8 +83,31 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(In in, Out out, long
     v += vals[q];
   }
   uint32_t ex;
-  block_exclusive_scan<kScanThreads>(v, ex, s_warp);
-  uint32_t run = bsum[blockIdx.x] + ex;
+  const uint32_t T = block_exclusive_scan<kScanThreads>(v, ex, s_warp);
+  if (threadIdx.x == 0) {
+    const unsigned long long hiA = (unsigned long long)((epoch << 2) | 1u) << 32;
+    const unsigned long long hiP = (unsigned long long)((epoch << 2) | 2u) << 32;
+    st_relaxed_u64(look + bid, (bid == 0 ? hiP : hiA) | T);
+    uint32_t excl = 0;
+    if (bid > 0) {
+      const unsigned long long* p = look + (bid - 1);
+      for (;;) {
+        unsigned long long sv;
+        do {
+          sv = ld_relaxed_u64(p);
+        } while ((uint32_t)(sv >> 34) != epoch || ((sv >> 32) & 3u) == 0u);
+        excl += (uint32_t)sv;
+        if (((sv >> 32) & 3u) == 2u) break;
+        --p;
+      }
+      st_relaxed_u64(look + bid, hiP | (excl + T));
+    }
+    if (excl + T < excl && overflow) *overflow = 1;
+    if ((long long)bid == nb - 1) *total = excl + T;
+    s_pre = excl;
+  }
+  __syncthreads();
+  uint32_t run = s_pre + ex;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q)
     if (base + q < n) {
