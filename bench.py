@@ -32,7 +32,9 @@ import numpy as np  # noqa: E402
 METRIC = "interlaced LF frames/s (4K, 100 views)"
 METRICS = {"C": METRIC, "A": "interlaced LF frames/s (256x144, 8 views)",
            "B": "interlaced LF frames/s (4K, 45 views)", "D": "interlaced LF frames/s (8K, 100 views)",
-           "E": "interlaced LF frames/s (4K, 45 views, 256 head-tracked poses)"}
+           "E": "interlaced LF frames/s (4K, 45 views, 256 head-tracked poses)",
+           "P2K": "interlaced LF frames/s (1440x2560 portrait, 63 views, s=16)",
+           "P4K": "interlaced LF frames/s (4K, 71 views, s=18)"}
 UNIT = "frames/s"
 # algorithmic FP32 operations per (subpixel, splat) evaluation of Eqs.9-10
 # (DESIGN.md §5): delta 2, quadratic form 8, x(-1/2) 1, exp 1, o*exp 1,
