@@ -118,6 +118,8 @@ struct cr_ctx {
   bool has_frame = false;
   int launches = 0;
   cudaEvent_t ev[6] = {};
+  cudaStream_t side = nullptr;     // forked stream for concurrent big-record emission
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
 };
@@ -399,6 +401,9 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
     return CR_ERR_CUDA;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (ensure(c, c->scalars, 64) != CR_OK) {
     delete c;
     return CR_ERR_OUT_OF_MEMORY;
@@ -418,6 +423,12 @@ void cr_destroy(cr_ctx* c) {
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
 }
@@ -677,6 +688,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   int G = 1;
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
+  const size_t cam_smem = (size_t)N * kCamStride * sizeof(float);  // cameras staged per CTA
   uint32_t nvis = 0;
   uint32_t drange_h[2] = {0u, 0u};
   int kbits = 0;  // bits of the cluster id in the compressed presort key
@@ -739,11 +751,11 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (nvis > 0) {
     // count in (k, depth, i) order: position-indexed counts and union slots
 #define CR_COUNTS(GG)                                                                         \
-  k_count<GG><<<bin_grid, kBinThreads, 0, str>>>(                                       \
+  k_count<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                       \
       rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),      \
       P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                                 \
   CR_LAUNCHED(c);                                                                             \
-  k_count_big<GG><<<bin_grid, kBinThreads, 0, str>>>(                                   \
+  k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                   \
       P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
       P_<uint32_t>(c->cnt))
     switch (G) {
@@ -772,11 +784,15 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   uint32_t *tA = P_<uint32_t>(c->pta), *pA = P_<uint32_t>(c->pva);
   uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
   if (P > 0) {
+    // big-footprint records are emitted on a forked stream, concurrently with
+    // k_emit_flat (disjoint output positions); joined before the tile sort
+    CR_CUDA(c, cudaEventRecord(c->ev_fork, str));
+    CR_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     k_emit_flat<<<(unsigned)std::min<long long>((nvis + 255) / 256, 148 * 16), 256, 0, str>>>(
         rec_sorted, P_<uint32_t>(c->offs), nvis, P, P_<uint4>(c->slots), tA, pA);
     CR_LAUNCHED(c);
 #define CR_EMITB(GG)                                                                        \
-  k_emit_big<GG><<<bin_grid, kBinThreads, 0, str>>>(                                        \
+  k_emit_big<GG><<<bin_grid, kBinThreads, cam_smem, c->side>>>(                              \
       rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->biglist), sc + 6, P_<float4>(c->mean4), \
       P_<float4>(c->geom), tA, pA)
     switch (G) {
@@ -789,6 +805,8 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     }
 #undef CR_EMITB
     CR_LAUNCHED(c);
+    CR_CUDA(c, cudaEventRecord(c->ev_join, c->side));
+    CR_CUDA(c, cudaStreamWaitEvent(str, c->ev_join, 0));
   }
   CR_TRACE(c, "offsets+emit");
   CR_CUDA(c, cudaEventRecord(c->ev[3], str));

@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
                                                        uint4* __restrict__ slots,
                                                        uint32_t* __restrict__ big,
                                                        uint32_t* __restrict__ n_big) {
-  __shared__ float s_cam[kMaxViews * kCamStride];
+  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
   __shared__ int s_src[kBinWarps][32];  // item-window position -> source lane
@@ -695,10 +695,11 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
 // slot bit by bit into a shared-memory window of kEmitWin pairs (rows
 // ascending, tiles ascending), then the warp copies the window out with
 // coalesced stores.  Window positions of records flagged overflow are left
-// to k_emit_big, which runs afterwards and overwrites them.  Grid-stride over
-// record blocks.
+// untouched for k_emit_big, which runs concurrently on a forked stream.
+// Grid-stride over record blocks.
 // ===========================================================================
 constexpr int kEmitWin = 256;
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;  // window position owned by a big record
 __global__ void __launch_bounds__(256) k_emit_flat(const uint32_t* __restrict__ rec_sorted,
                                                    const uint32_t* __restrict__ offs, uint32_t n,
                                                    uint32_t P, const uint4* __restrict__ slots,
@@ -724,6 +725,9 @@ __global__ void __launch_bounds__(256) k_emit_flat(const uint32_t* __restrict__ 
     const uint32_t nrows = (h.x >> 16) & 0xFFu;
     const uint32_t lo = o - f0, hi = o1 - f0;  // local pair range
     for (uint32_t wb = 0; wb < f1 - f0; wb += kEmitWin) {  // warp-uniform
+#pragma unroll
+      for (int q = 0; q < kEmitWin / 32; ++q) s_t[w][q * 32 + lane] = kNoTile;
+      __syncwarp();
       if (dec && hi > wb && lo < wb + kEmitWin) {
         uint32_t q = lo;
         for (uint32_t t = 0; t < nrows && q < wb + kEmitWin; t += 2) {
@@ -751,7 +755,9 @@ __global__ void __launch_bounds__(256) k_emit_flat(const uint32_t* __restrict__ 
       __syncwarp();
       const uint32_t nw = min((uint32_t)kEmitWin, f1 - f0 - wb);
       for (uint32_t i = (uint32_t)lane; i < nw; i += 32u) {
-        out_t[f0 + wb + i] = s_t[w][i];
+        const uint32_t t = s_t[w][i];
+        if (t == kNoTile) continue;  // a big record's position: k_emit_big writes it
+        out_t[f0 + wb + i] = t;
         out_v[f0 + wb + i] = s_v[w][i];
       }
       __syncwarp();
@@ -771,7 +777,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __res
                                                            const float4* __restrict__ mean4,
                                                            const float4* __restrict__ geom,
                                                            uint32_t* __restrict__ cnt) {
-  __shared__ float s_cam[kMaxViews * kCamStride];
+  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr,
     const float4* __restrict__ mean4, const float4* __restrict__ geom,
     uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
-  __shared__ float s_cam[kMaxViews * kCamStride];
+  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
   __shared__ uint32_t s_rows[kBinWarps][kMaxRows];
   stage_cams(s_cam);
   __syncthreads();
