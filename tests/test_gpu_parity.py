@@ -353,3 +353,33 @@ def test_fullframe_baseline_equals_subpixel_s1(cfgA_pair):
     from paper_2605_04509_b200._native import CrError
     with pytest.raises(CrError, match="INVALID_CONFIG"):
         g.render(8, fullframe=True)
+
+
+@pytest.mark.parametrize("s", [16, 18, 3])
+def test_large_and_odd_clusters(s):
+    """Cluster sizes beyond 8: G = 16 (P2K's s=16) and G = 32 (P4K's s=18)
+    lane groups, and a non-power-of-two s=3 (G=4 with an idle lane), against
+    the oracle: bit-exact keys/ranges/counts, image tolerance; plus a band."""
+    _need_gpu()
+    W, H, N = 192, 112, 40
+    sc = sy.random_scene(3000, 1, seed=21, scale_median=0.035)
+    cams = sy.orbit_rig(N, 20.0, W, H, radius=3.0, height=0.3, fov_y_deg=50.0)
+    g, o = make_pair(sc, W, H, N, 13.7, 0.19, 2.1, cams)
+    check_frame(g, o, s)
+    check_frame(g, o, s, rows=(2, 5))
+
+
+def test_big_footprints_general_path():
+    """Records beyond the 64-byte union slot (> 6 union rows or >= 64 tile
+    columns) take the warp-wide general path (k_count_big / k_emit_big):
+    large splats on a wide panel, bit-exact against the oracle."""
+    _need_gpu()
+    W, H, N = 1280, 112, 12
+    sc = sy.random_scene(600, 0, seed=5, scale_median=0.25)
+    cams = sy.orbit_rig(N, 12.0, W, H, radius=3.0, height=0.2, fov_y_deg=30.0)
+    g, o = make_pair(sc, W, H, N, 10.9, 0.21, 0.7, cams)
+    for s in (4, 12):
+        check_frame(g, o, s)
+        g.render(cluster_size=s, stats=True)
+        assert g.last_stats["emit_fallback"] > 0, "general path not exercised"
+    check_frame(g, o, 4, rows=(1, 5))
