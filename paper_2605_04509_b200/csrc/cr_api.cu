@@ -69,6 +69,13 @@ struct Scan {  // functors for the generic device scan
   struct InArr {
     const uint32_t* a;
     __device__ uint32_t operator()(long long i) const { return a[i]; }
+    // 8 consecutive elements from i (i % 8 == 0, i + 8 <= n): two 16-byte loads
+    __device__ void load8(long long i, uint32_t* v) const {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + i));
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(a + i) + 1);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+      v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    }
   };
   struct OutStore {
     uint32_t* o;

@@ -64,6 +64,46 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Decoupled look-back over the predecessors' status words at p, p - stride,
+// p - 2*stride, ... (tile b-1, b-2, ...): four independent loads per round,
+// consumed in order (a not-yet-published word is re-polled), so the walk
+// over aggregate-only predecessors costs a quarter of the dependent L2 round
+// trips.  Returns the exclusive prefix; tile 0 always publishes inclusive.
+__device__ __forceinline__ uint32_t lookback4(const unsigned long long* p, long long avail,
+                                              long long stride, uint32_t epoch) {
+  uint32_t excl = 0;
+  for (;;) {
+    unsigned long long sv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[q] = q < avail ? ld_status(p - q * stride) : 0ull;
+    int q = 0;
+    for (; q < 4 && q < avail; ++q) {
+      const unsigned long long s = sv[q];
+      if ((uint32_t)(s >> 34) != epoch || ((s >> 32) & 3u) == 0u) break;  // not ready: re-poll
+      excl += (uint32_t)s;
+      if (((s >> 32) & 3u) == 2u) return excl;
+    }
+    p -= q * stride;
+    avail -= q;
+  }
+}
+
+
+// inputs that can load 8 consecutive elements at once (vectorized)
+template <class T, class = void>
+struct HasLoad8 { static constexpr bool value = false; };
+template <class T>
+struct HasLoad8<T, decltype(void(&T::load8))> { static constexpr bool value = true; };
+
 template <class In, class Out>
 __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
     In in, Out out, long long n, unsigned long long* __restrict__ look,
@@ -77,11 +117,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
   const long long nb = (n + kScanTile - 1) / kScanTile;
   const long long base = (long long)bid * kScanTile + (long long)threadIdx.x * kScanItems;
   uint32_t vals[kScanItems], v = 0;
+  if constexpr (HasLoad8<In>::value) {
+    static_assert(kScanItems == 8, "load8 reads 8 elements");
+    if (base + kScanItems <= n) {
+      in.load8(base, vals);
+    } else {
 #pragma unroll
-  for (int q = 0; q < kScanItems; ++q) {
-    vals[q] = (base + q < n) ? in(base + q) : 0u;
-    v += vals[q];
+      for (int q = 0; q < kScanItems; ++q) vals[q] = (base + q < n) ? in(base + q) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) vals[q] = (base + q < n) ? in(base + q) : 0u;
   }
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) v += vals[q];
   uint32_t ex;
   const uint32_t T = block_exclusive_scan<kScanThreads>(v, ex, s_warp);
   if (threadIdx.x == 0) {
@@ -90,16 +139,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
     st_relaxed_u64(look + bid, (bid == 0 ? hiP : hiA) | T);
     uint32_t excl = 0;
     if (bid > 0) {
-      const unsigned long long* p = look + (bid - 1);
-      for (;;) {
-        unsigned long long sv;
-        do {
-          sv = ld_relaxed_u64(p);
-        } while ((uint32_t)(sv >> 34) != epoch || ((sv >> 32) & 3u) == 0u);
-        excl += (uint32_t)sv;
-        if (((sv >> 32) & 3u) == 2u) break;
-        --p;
-      }
+      excl = lookback4(look + (bid - 1), (long long)bid, 1, epoch);
       st_relaxed_u64(look + bid, hiP | (excl + T));
     }
     if (excl + T < excl && overflow) *overflow = 1;
@@ -361,15 +401,6 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
   }
 }
 
-__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // one stable pass on digit (key >> shift) & 255; ghist = this digit's global
 // histogram; look = [tiles][256] status words; ctr = tile counter (zeroed).
 // Ranks by 8-ballot multisplit peers (measured faster than match.any.sync on
@@ -441,16 +472,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   // look back for the exclusive prefix of digit d over the preceding tiles
   uint32_t excl = 0;
   if (bid > 0) {
-    const unsigned long long* p = look + (size_t)(bid - 1) * 256 + d;
-    for (;;) {
-      unsigned long long s;
-      do {
-        s = ld_status(p);
-      } while ((uint32_t)(s >> 34) != epoch || ((s >> 32) & 3u) == 0u);
-      excl += (uint32_t)s;
-      if (((s >> 32) & 3u) == 2u) break;
-      p -= 256;
-    }
+    excl = lookback4(look + (size_t)(bid - 1) * 256 + d, (long long)bid, 256, epoch);
     st_status(my, hiP | (excl + acc));
   }
   __syncthreads();
