@@ -1,8 +1,9 @@
-"""A/B timing of CR_EXP kernel variants: python tools/exp_variants.py C 0 1 2 4 ...
+"""A/B timing harness: python tools/exp_variants.py C 0 [1 2 ...]
 
-Renders the config with each CR_EXP bit mask (read by cr_render_interlaced per
-call), prints median per-stage ms and whether the image AND the sorted pairs
-equal those of the first variant (all variants must be bit-identical)."""
+Renders the config with each value of the CR_EXP environment variable (an
+experiment knob a kernel-variant A/B build can read in cr_render_interlaced;
+the committed library ignores it), prints median per-stage ms and whether the
+image equals the first variant's (variants must be bit-identical)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
