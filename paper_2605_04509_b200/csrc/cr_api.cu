@@ -129,6 +129,7 @@ struct cr_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
+  int exp = 0;         // CR_EXP: kernel-variant A/B experiments (read per render)
 };
 
 namespace {
@@ -636,6 +637,10 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (R > 0xFFFFFFFFLL) return fail(c, CR_ERR_CAPACITY, "K*M = %lld exceeds 2^32", R);
   cudaSetDevice(c->device);
   c->launches = 0;
+  {
+    const char* ex = getenv("CR_EXP");
+    c->exp = ex ? atoi(ex) : 0;
+  }
   c->has_frame = false;
   cudaStream_t str = c->stream;
 

@@ -192,10 +192,11 @@ __global__ void k_upload(long long M, int nc3, const float* __restrict__ means,
 }
 
 // ===========================================================================
-// Cameras staged in shared memory (stride 17 floats: the <= 32 distinct views
-// read by one warp hit distinct banks).
+// Cameras staged in shared memory with an 80-byte stride (20 floats): the 8
+// consecutive cameras a G=8 lane group reads hit 8 distinct 16-byte bank
+// groups, and each camera is 4 x LDS.128.
 // ===========================================================================
-constexpr int kCamStride = 17;
+constexpr int kCamStride = 20;
 __device__ __forceinline__ void stage_cams(float* s_cam) {
   const int N = c_fp.N;
   for (int q = threadIdx.x; q < N * 16; q += blockDim.x) {
@@ -204,12 +205,13 @@ __device__ __forceinline__ void stage_cams(float* s_cam) {
   }
 }
 __device__ __forceinline__ CamDev load_cam(const float* s_cam, int j) {
+  const float4* q4 = reinterpret_cast<const float4*>(s_cam + j * kCamStride);
+  const float4 c0 = q4[0], c1 = q4[1], c2 = q4[2], c3 = q4[3];
   CamDev c;
-  const float* p = s_cam + j * kCamStride;
-#pragma unroll
-  for (int f = 0; f < 9; ++f) c.R[f] = p[f];
-  c.t[0] = p[9]; c.t[1] = p[10]; c.t[2] = p[11];
-  c.fx = p[12]; c.fy = p[13]; c.cx = p[14]; c.cy = p[15];
+  c.R[0] = c0.x; c.R[1] = c0.y; c.R[2] = c0.z; c.R[3] = c0.w;
+  c.R[4] = c1.x; c.R[5] = c1.y; c.R[6] = c1.z; c.R[7] = c1.w;
+  c.R[8] = c2.x; c.t[0] = c2.y; c.t[1] = c2.z; c.t[2] = c2.w;
+  c.fx = c3.x; c.fy = c3.y; c.cx = c3.z; c.cy = c3.w;
   return c;
 }
 
@@ -536,6 +538,9 @@ struct BinWarpSmem {
 // recs is the depth-sorted record list and every output is indexed by the list
 // position g (cnt[g], slot g, big list of positions), so the offsets scan and
 // the emission read them sequentially.
+// The group's lanes write the union slot (one uint4 each); item lanes read
+// their source lane's / group's data from shared memory (measured: -0.25 ms
+// at config C against the lead-writes + 13-shuffle version).
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
                                                        uint32_t n,
@@ -549,6 +554,8 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
   __shared__ int s_src[kBinWarps][32];  // item-window position -> source lane
+  __shared__ float4 s_lv[kBinWarps][32];     // per lane: mx, my, first, seg0
+  __shared__ float4 s_gv[kBinWarps][32][2];  // per group: ellipse constants, rmin
   stage_cams(s_cam);
   __syncthreads();
   constexpr int GPW = 32 / G;  // groups (records) per warp
@@ -614,6 +621,11 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
     }
     const int total = __shfl_sync(0xffffffffu, pre, 31);
     const int seg0 = pre - ni;  // this lane's first item
+    s_lv[w][lane] = make_float4(mx, my, __int_as_float(first), __int_as_float(seg0));
+    if (lead) {
+      s_gv[w][gi][0] = make_float4(el.ex, el.ey, el.dyR, el.tc);
+      s_gv[w][gi][1] = make_float4(el.ic, el.b, el.det, __int_as_float(rmin));
+    }
     __syncwarp();
     // ---- (view, row) items, 32 per window: lane i takes item base+i
     for (int base = 0; base < total; base += 32) {
@@ -628,20 +640,16 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
       const unsigned mk = marks & upto;
       __syncwarp();
       const int src = (idx < total && mk) ? s_src[w][31 - __clz(mk)] : 0;
-      const float smx = __shfl_sync(0xffffffffu, mx, src);
-      const float smy = __shfl_sync(0xffffffffu, my, src);
-      const int sfirst = __shfl_sync(0xffffffffu, first, src);
-      const int sseg0 = __shfl_sync(0xffffffffu, seg0, src);
-      const int srmin = __shfl_sync(0xffffffffu, rmin, src);
+      // the source lane's / group's data from shared memory
+      const float4 lv = s_lv[w][src];
+      const float4 g0 = s_gv[w][src / G][0], g1 = s_gv[w][src / G][1];
+      const float smx = lv.x, smy = lv.y;
+      const int sfirst = __float_as_int(lv.z), sseg0 = __float_as_int(lv.w);
+      const int srmin = __float_as_int(g1.w);
       const int slo = __shfl_sync(0xffffffffu, lo_ref, src);
       EllRec e;
-      e.ex = __shfl_sync(0xffffffffu, el.ex, src);
-      e.ey = __shfl_sync(0xffffffffu, el.ey, src);
-      e.dyR = __shfl_sync(0xffffffffu, el.dyR, src);
-      e.tc = __shfl_sync(0xffffffffu, el.tc, src);
-      e.ic = __shfl_sync(0xffffffffu, el.ic, src);
-      e.b = __shfl_sync(0xffffffffu, el.b, src);
-      e.det = __shfl_sync(0xffffffffu, el.det, src);
+      e.ex = g0.x; e.ey = g0.y; e.dyR = g0.z; e.tc = g0.w;
+      e.ic = g1.x; e.b = g1.y; e.det = g1.z;
       if (idx < total) {
         const int gs = src / G;
         const int row = sfirst + (idx - sseg0);
@@ -666,7 +674,23 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
     const bool slow = active && nrows > 0 && (!fast || s_flag[w][gi] != 0);
     uint32_t c = 0;
     const unsigned long long o = g;  // output index: list position
-    if (active && fast && !slow && lead) {
+    if (G >= 8) {  // the group's lanes write the slot (needs >= kSlotRows lanes)
+      // the group's lanes 0..3 each write one uint4 of the slot; lanes 0..5 count a row
+      const bool wr = active && fast && !slow;
+      uint32_t pc = (wr && v < kSlotRows) ? (uint32_t)__popcll(s_mask[w][gi][v]) : 0u;
+#pragma unroll
+      for (int q = 1; q < G; q <<= 1) pc += __shfl_xor_sync(0xffffffffu, pc, q);
+      if (wr) c = pc;
+      if (wr && v < 4) {
+        uint4 val;
+        if (v == 0) {
+          val = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
+        } else {
+          val = *reinterpret_cast<const uint4*>(&s_mask[w][gi][2 * (v - 1)]);
+        }
+        slots[4ull * o + v] = val;
+      }
+    } else if (active && fast && !slow && lead) {
       unsigned long long mk[kSlotRows];
 #pragma unroll
       for (int t = 0; t < kSlotRows; ++t) {
