@@ -272,9 +272,12 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
                                 float muy, float muz, const EllRec& el, int it0, int istep,
                                 uint32_t* __restrict__ row_cnt, const uint32_t* __restrict__ row_off,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
-                                uint32_t payload, uint32_t cap = 0xFFFFFFFFu) {
+                                uint32_t payload, unsigned long long* __restrict__ row_mask = nullptr,
+                                int* __restrict__ row_wlo = nullptr, int* __restrict__ wide = nullptr) {
   // MODE 0: count the group's rows; MODE 3: also store per-row counts in
-  // row_cnt[it]; MODE 2: write the tiles of row it at row_off[it] + rank.
+  // row_cnt[it] (and, with row_mask, the row's 64-column window mask and the
+  // tile id of its bit 0; *wide = 1 if a row needs more than one window);
+  // MODE 2: write the tiles of row it at row_off[it] + rank.
   // The group handles union rows it = it0, it0 + istep, ...
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int j = k * s + v;
@@ -336,16 +339,19 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
           const int pl = __popc(lo32);
           for (int q = (int)(threadIdx.x & (G - 1)); q < pc; q += G) {
             const int bit = q < pl ? nth_set_bit(lo32, q) : 32 + nth_set_bit(hi32, q - pl);
-            if (rowpos + q < cap) {  // capacity guard (the host re-runs with the exact size)
-              out_t[rowpos + q] = rowbase + (uint32_t)(wlo + bit);
-              out_v[rowpos + q] = payload;
-            }
+            out_t[rowpos + q] = rowbase + (uint32_t)(wlo + bit);
+            out_v[rowpos + q] = payload;
           }
           rowpos += (uint32_t)pc;
         }
         rown += (uint32_t)pc;
+        if (MODE == 3 && row_mask && lead && rowok && wi == 0) {
+          row_mask[it] = mask;
+          row_wlo[it] = (int)(rowbase + (uint32_t)wlo);  // tile id of the mask's bit 0
+        }
       }
     }
+    if (MODE == 3 && row_mask && lead && rowok && nwin > 1) *wide = 1;
     if (MODE == 3 && lead && rowok) row_cnt[it] = rown;
     n += rown;
   }
@@ -829,14 +835,17 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr,
     const float4* __restrict__ mean4, const float4* __restrict__ geom,
     uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
-  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
+  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic)
   __shared__ uint32_t s_rows[kBinWarps][kMaxRows];
+  __shared__ unsigned long long s_rmask[kBinWarps][kMaxRows];  // per row: window mask
+  __shared__ int s_rwlo[kBinWarps][kMaxRows];                  // per row: window column
+  __shared__ int s_wide[kBinWarps];
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
   constexpr int GPW = 32 / G;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
-  uint32_t* rows = s_rows[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
+  uint32_t* rows = s_rows[w];
   const uint32_t nwarps = gridDim.x * kBinWarps;
   for (uint32_t g = (blockIdx.x * kBinThreads + threadIdx.x) / 32; g < n; g += nwarps) {
     const uint32_t e = elist[g];
@@ -845,12 +854,15 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
     const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
     for (int q = lane; q < kMaxRows; q += 32) rows[q] = 0;
+    if (lane == 0) s_wide[w] = 0;
     __syncwarp();
+    // per-row counts and window masks (rows relative to the union's first row)
     group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
-                      nullptr, 0);
+                      nullptr, 0, s_rmask[w], s_rwlo[w], &s_wide[w]);
     __syncwarp();
     // exclusive scan of the per-row counts -> row offsets (in place)
     uint32_t carry = offs[e];
+    int nrows = 0;
     for (int b0 = 0; b0 < kMaxRows; b0 += 32) {
       const uint32_t x = rows[b0 + lane];
       uint32_t incl = x;
@@ -861,10 +873,28 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
       }
       rows[b0 + lane] = carry + incl - x;
       carry += __shfl_sync(0xffffffffu, incl, 31);
+      nrows = max(nrows, __reduce_max_sync(0xffffffffu, x ? b0 + lane + 1 : 0));
     }
     __syncwarp();
-    group_union<2, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, rows, out_t, out_v,
-                      r);
+    if (s_wide[w]) {  // a row wider than one 64-column window: recompute and write
+      group_union<2, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, rows, out_t,
+                        out_v, r);
+    } else {  // every row from its stored window mask (no second union): lane per row
+      for (int it = lane; it < nrows; it += 32) {
+        uint32_t pos = rows[it];
+        const uint32_t end = it + 1 < nrows ? rows[it + 1] : carry;
+        if (end == pos) continue;  // empty row (its mask slot was not written)
+        unsigned long long mk = s_rmask[w][it];
+        const uint32_t tb = (uint32_t)s_rwlo[w][it];
+        while (mk) {
+          const int bit = __ffsll((long long)mk) - 1;
+          mk &= mk - 1;
+          out_t[pos] = tb + (uint32_t)bit;
+          out_v[pos] = r;
+          ++pos;
+        }
+      }
+    }
     __syncwarp();
   }
 }
