@@ -52,8 +52,7 @@ struct Scan {  // functors for the generic device scan
     uint32_t* vo;
     const uint32_t* drange;
     int kbits;
-    __device__ void operator()(long long i, uint32_t ex, uint32_t v) const {
-      if (!v) return;
+    __device__ uint2 stage(long long i) const {  // flagged element i -> (key, r)
       const uint32_t r = (uint32_t)i;
       const uint32_t d = dkey[r], lo = drange[0], span = drange[1] - lo;
       const int B = span ? 32 - __clz(span) : 1;
@@ -62,8 +61,11 @@ struct Scan {  // functors for the generic device scan
         key = d - lo;
         if (kbits) key |= fdiv(r, c_fp.divM) << B;
       }
-      ko[ex] = key;
-      vo[ex] = r;
+      return make_uint2(key, r);
+    }
+    __device__ void put(uint32_t pos, uint2 kv) const {
+      ko[pos] = kv.x;
+      vo[pos] = kv.y;
     }
   };
   struct InArr {
@@ -80,6 +82,11 @@ struct Scan {  // functors for the generic device scan
   struct OutStore {
     uint32_t* o;
     __device__ void operator()(long long i, uint32_t ex, uint32_t) const { o[i] = ex; }
+    __device__ void store8(long long i, const uint32_t* ex) const {  // i % 8 == 0
+      uint4* p = reinterpret_cast<uint4*>(o + i);
+      p[0] = make_uint4(ex[0], ex[1], ex[2], ex[3]);
+      p[1] = make_uint4(ex[4], ex[5], ex[6], ex[7]);
+    }
   };
 };
 

@@ -104,6 +104,19 @@ struct HasLoad8 { static constexpr bool value = false; };
 template <class T>
 struct HasLoad8<T, decltype(void(&T::load8))> { static constexpr bool value = true; };
 
+// outputs that compact flagged elements to (u32, u32) pairs: staged in shared
+// memory by block-local rank and written out coalesced (stage(i) -> pair,
+// put(global position, pair))
+template <class T, class = void>
+struct HasStage { static constexpr bool value = false; };
+template <class T>
+struct HasStage<T, decltype(void(&T::stage))> { static constexpr bool value = true; };
+// outputs that store the 8 exclusive prefixes of a thread at once
+template <class T, class = void>
+struct HasStore8 { static constexpr bool value = false; };
+template <class T>
+struct HasStore8<T, decltype(void(&T::store8))> { static constexpr bool value = true; };
+
 template <class In, class Out>
 __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
     In in, Out out, long long n, unsigned long long* __restrict__ look,
@@ -147,13 +160,38 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
     s_pre = excl;
   }
   __syncthreads();
-  uint32_t run = s_pre + ex;
+  if constexpr (HasStage<Out>::value) {  // flags -> compacted pairs, coalesced writes
+    __shared__ uint2 s_kv[kScanTile];
+    uint32_t loc = ex;
 #pragma unroll
-  for (int q = 0; q < kScanItems; ++q)
-    if (base + q < n) {
-      out(base + q, run, vals[q]);
+    for (int q = 0; q < kScanItems; ++q)
+      if (base + q < n && vals[q]) s_kv[loc++] = out.stage(base + q);
+    __syncthreads();
+    const uint32_t pre = s_pre;
+    for (uint32_t p = threadIdx.x; p < T; p += kScanThreads) out.put(pre + p, s_kv[p]);
+  } else if constexpr (HasStore8<Out>::value) {
+    uint32_t run = s_pre + ex, ex8[kScanItems];
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) {
+      ex8[q] = run;
       run += vals[q];
     }
+    if (base + kScanItems <= n) {
+      out.store8(base, ex8);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kScanItems; ++q)
+        if (base + q < n) out(base + q, ex8[q], vals[q]);
+    }
+  } else {
+    uint32_t run = s_pre + ex;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q)
+      if (base + q < n) {
+        out(base + q, run, vals[q]);
+        run += vals[q];
+      }
+  }
 }
 
 // ----------------------------------------------------------------- radix
