@@ -718,6 +718,181 @@ __global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restric
   }
 }
 
+// k_count2: as k_count, but every lane owns TWO views of its record (views
+// v*2 and v*2+1 of the cluster), so a G-lane group covers 2G views and a warp
+// takes 32/G records per step: the per-record share of loads, group
+// reductions, the item prefix scan and the slot write halves.  Same per-view
+// exact arithmetic, same union, same slot.
+template <int G>
+__global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restrict__ recs,
+                                                        uint32_t n,
+                                                        const float4* __restrict__ mean4,
+                                                        const float4* __restrict__ geom,
+                                                        uint32_t* __restrict__ cnt,
+                                                        uint4* __restrict__ slots,
+                                                        uint32_t* __restrict__ big,
+                                                        uint32_t* __restrict__ n_big) {
+  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic)
+  __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
+  __shared__ int s_flag[kBinWarps][32];
+  __shared__ int s_src[kBinWarps][32];
+  __shared__ float4 s_lv[kBinWarps][32];     // per lane: view A mx, my, first; seg0
+  __shared__ float4 s_lv2[kBinWarps][32];    // per lane: view B mx, my, first; ni of A
+  __shared__ float4 s_gv[kBinWarps][32][2];  // per group: ellipse constants, rmin
+  stage_cams(s_cam);
+  __syncthreads();
+  constexpr int GPW = 32 / G;
+  const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
+  const bool lead = v == 0;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
+       wb < n; wb += nwarps * GPW) {  // warp-uniform loop
+    const unsigned long long g = wb + gi;
+    const bool active = g < n;
+    uint32_t r = 0;
+    float4 m = make_float4(0.f, 0.f, 0.f, 1.f);
+    float4 q0 = make_float4(1.f, 1.f, 0.f, 1.f), q1 = make_float4(1.f, 0.f, 1.f, 0.f);
+    int k = 0;
+    if (active) {
+      r = recs[g];
+      k = (int)fdiv(r, c_fp.divM);
+      m = mean4[(long long)r - (long long)k * c_fp.M];
+      q0 = geom[2ull * r];
+      q1 = geom[2ull * r + 1];
+    }
+    const EllRec el = ell_load(q0, q1);
+    // ---- the lane's two views: exact means (Eq.5) and AccuTile rows (O7)
+    float mx[2] = {0.f, 0.f}, my[2] = {0.f, 0.f};
+    int ty0[2] = {0x7fffffff, 0x7fffffff}, ty1[2] = {-1, -1};
+    bool vis[2] = {false, false};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int vv = 2 * v + u;
+      const int j = k * s + vv;
+      if (active && vv < s && j < N) {
+        const CamDev cam = load_cam(s_cam, j);
+        const F3 p = cam_point_exact(cam, m.x, m.y, m.z);
+        if (p.z >= c_fp.znear) {
+          mean2d_exact(cam, p, mx[u], my[u]);
+          view_rows(el, my[u], TY, ty0[u], ty1[u]);
+          vis[u] = true;
+        }
+      }
+    }
+    const int rmin = max(gmin<G>(min(vis[0] ? ty0[0] : 0x7fffffff, vis[1] ? ty0[1] : 0x7fffffff)),
+                         c_fp.row0);
+    const int rmax = min(gmax<G>(max(vis[0] ? ty1[0] : -1, vis[1] ? ty1[1] : -1)), c_fp.row1 - 1);
+    const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
+    int kl = 0x7f800000;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int xk = __float_as_int(mx[u]);
+      if (vis[u]) kl = min(kl, xk ^ ((xk >> 31) & 0x7fffffff));
+    }
+    const int kmin = gmin<G>(kl);
+    const float mxlo = __int_as_float(kmin ^ ((kmin >> 31) & 0x7fffffff));
+    const int lo_ref = (int)fmaxf(floorf((mxlo - el.ex - 15.5f) * 0.0625f) - 1.0f, -1.0f);
+    const bool fast = nrows > 0 && nrows <= kSlotRows;
+    int nv[2] = {0, 0}, first[2] = {0, 0};
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (fast && vis[u]) {
+        first[u] = max(ty0[u], rmin);
+        nv[u] = max(0, min(ty1[u], rmax) - first[u] + 1);
+      }
+    const int ni = nv[0] + nv[1];
+    if (lead) {
+      s_flag[w][gi] = 0;
+#pragma unroll
+      for (int t = 0; t < kSlotRows; ++t) s_mask[w][gi][t] = 0ull;
+    }
+    int pre = ni;  // warp inclusive prefix of (view,row) items
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    const int seg0 = pre - ni;
+    s_lv[w][lane] = make_float4(mx[0], my[0], __int_as_float(first[0]), __int_as_float(seg0));
+    s_lv2[w][lane] = make_float4(mx[1], my[1], __int_as_float(first[1]), __int_as_float(nv[0]));
+    if (lead) {
+      s_gv[w][gi][0] = make_float4(el.ex, el.ey, el.dyR, el.tc);
+      s_gv[w][gi][1] = make_float4(el.ic, el.b, el.det, __int_as_float(rmin));
+    }
+    __syncwarp();
+    for (int base = 0; base < total; base += 32) {
+      const bool inter = ni > 0 && pre > base && seg0 < base + 32;
+      const int spos = max(seg0, base) - base;
+      if (inter) s_src[w][spos] = lane;
+      const unsigned marks = __reduce_or_sync(0xffffffffu, inter ? (1u << spos) : 0u);
+      const int idx = base + lane;
+      const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+      const unsigned mk = marks & upto;
+      __syncwarp();
+      const int src = (idx < total && mk) ? s_src[w][31 - __clz(mk)] : 0;
+      const float4 la = s_lv[w][src], lb = s_lv2[w][src];
+      const int loc = idx - __float_as_int(la.w);  // item index within the source lane
+      const bool inb = loc >= __float_as_int(lb.w);
+      const float smx = inb ? lb.x : la.x, smy = inb ? lb.y : la.y;
+      const int row = inb ? __float_as_int(lb.z) + (loc - __float_as_int(lb.w))
+                          : __float_as_int(la.z) + loc;
+      const float4 g0 = s_gv[w][src / G][0], g1 = s_gv[w][src / G][1];
+      const int srmin = __float_as_int(g1.w);
+      const int slo = __shfl_sync(0xffffffffu, lo_ref, src);
+      EllRec e;
+      e.ex = g0.x; e.ey = g0.y; e.dyR = g0.z; e.tc = g0.w;
+      e.ic = g1.x; e.b = g1.y; e.det = g1.z;
+      if (idx < total) {
+        const int gs = src / G;
+        int tx0, tx1;
+        if (view_row_cols(e, smx, smy, row, TX, tx0, tx1) && tx0 <= tx1) {
+          if (tx0 < slo || tx1 - slo >= 64) {
+            atomicOr(&s_flag[w][gs], 1);
+          } else {
+            const int len = tx1 - tx0 + 1;
+            const unsigned long long bits =
+                ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - slo);
+            unsigned* mw = reinterpret_cast<unsigned*>(&s_mask[w][gs][row - srmin]);
+            if ((unsigned)bits) atomicOr(mw, (unsigned)bits);
+            if ((unsigned)(bits >> 32)) atomicOr(mw + 1, (unsigned)(bits >> 32));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // ---- finalize: the group's lanes write the slot; general path for the rest
+    const bool slow = active && nrows > 0 && (!fast || s_flag[w][gi] != 0);
+    uint32_t c = 0;
+    const unsigned long long o = g;
+    {
+      const bool wr = active && fast && !slow;
+      uint32_t pc = 0;
+      if (wr)
+        for (int t = v; t < kSlotRows; t += G) pc += (uint32_t)__popcll(s_mask[w][gi][t]);
+#pragma unroll
+      for (int q = 1; q < G; q <<= 1) pc += __shfl_xor_sync(0xffffffffu, pc, q);
+      if (wr) c = pc;
+      for (int q = v; wr && q < 4; q += G) {
+        uint4 val;
+        if (q == 0) {
+          val = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
+        } else {
+          val = *reinterpret_cast<const uint4*>(&s_mask[w][gi][2 * (q - 1)]);
+        }
+        slots[4ull * o + q] = val;
+      }
+    }
+    if (slow && lead) {  // footprint beyond the fast path: k_count_big
+      slots[4ull * o] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
+      big[atomicAdd(n_big, 1u)] = (uint32_t)o;
+    }
+    if (active && lead) cnt[o] = c;
+    __syncwarp();
+  }
+}
+
 // ===========================================================================
 // a6 emit, fast path over the depth-sorted, position-indexed slots (k_count
 // SORTED): each warp takes 32 consecutive records (lane = record), whose pairs
