@@ -770,12 +770,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (nvis > 0) {
     // count in (k, depth, i) order: position-indexed counts and union slots
 #define CR_COUNTS(GG)                                                                         \
-  if (GG >= 8) /* two views per lane (measured: bin 7.56 -> 6.58 ms at config C) */           \
-    k_count2<(GG >= 8 ? GG / 2 : 1)><<<bin_grid, kBinThreads, cam_smem, str>>>(               \
+  if (GG >= 8) /* two views per lane */                                                       \
+    k_countv<(GG >= 8 ? GG / 2 : 1), 2><<<bin_grid, kBinThreads, cam_smem, str>>>(            \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
         P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
   else                                                                                        \
-    k_count<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                     \
+    k_countv<GG, 1><<<bin_grid, kBinThreads, cam_smem, str>>>(                                 \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
         P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
   CR_LAUNCHED(c);                                                                             \

@@ -519,212 +519,30 @@ __global__ void __launch_bounds__(128) k_preprocess(
 }
 
 // ===========================================================================
-// a6 count — per warp, 32/G records (one G-lane group each, lane = view).
-// Fast path (footprint <= kSlotRows rows, < 64 columns from a conservative
-// reference column lo_ref): the (view, row) items of all the warp's records
-// are redistributed evenly over the 32 lanes (warp prefix + binary search),
-// each item computes its exact AccuTile interval (O7) and ORs it into the
-// record's per-row 64-bit mask in shared memory.  The record's union slot
-// (64 B: header, lo_ref, up to kSlotRows masks) is written for the emit pass.
-// Records outside the fast path take group_union (general, same set) and are
-// flagged in their slot.  Grid-stride, warp-uniform loop; cameras in smem.
+// a6 count — per warp, 32/G records (one G-lane group each; every lane owns
+// VPL consecutive views of its record).  Fast path (footprint <= kSlotRows
+// rows, < 64 columns from a conservative reference column lo_ref): the
+// (view, row) items of all the warp's records are redistributed evenly over
+// the 32 lanes (segment-start marks + clz source lookup, source data staged
+// in shared memory), each item computes its exact AccuTile interval (O7) and
+// ORs it into the record's per-row 64-bit mask in shared memory; the group's
+// lanes write the record's 64-byte union slot (header, lo_ref, up to
+// kSlotRows masks) at its depth-sorted list position g for the emit pass.
+// Records outside the fast path are flagged in their slot and listed for
+// k_count_big.  recs is the depth-sorted record list; every output is indexed
+// by the list position (cnt[g], slot g, big list of positions), so the offsets
+// scan and the emission read them sequentially.  Grid-stride, warp-uniform
+// loop; cameras in shared memory.
 // ===========================================================================
 constexpr int kBinThreads = 256;
 constexpr int kBinWarps = kBinThreads / 32;
 
-struct BinWarpSmem {
-  float mx[32], my[32];
-  int row0[32];                               // first covered row of each view lane
-  int pre[32];                                // inclusive prefix of items per lane
-  float ell[32][8];                           // per group: ex, ey, dyR, tc, ic, b, det
-  int rmin[32], lo_ref[32], flag[32];
-  unsigned long long mask[32][kSlotRows];     // per group, per row
-};
-
-// recs is the depth-sorted record list and every output is indexed by the list
-// position g (cnt[g], slot g, big list of positions), so the offsets scan and
-// the emission read them sequentially.
-// The group's lanes write the union slot (one uint4 each); item lanes read
-// their source lane's / group's data from shared memory (measured: -0.25 ms
-// at config C against the lead-writes + 13-shuffle version).
-template <int G>
-__global__ void __launch_bounds__(kBinThreads) k_count(const uint32_t* __restrict__ recs,
-                                                       uint32_t n,
-                                                       const float4* __restrict__ mean4,
-                                                       const float4* __restrict__ geom,
-                                                       uint32_t* __restrict__ cnt,
-                                                       uint4* __restrict__ slots,
-                                                       uint32_t* __restrict__ big,
-                                                       uint32_t* __restrict__ n_big) {
-  extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
-  __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
-  __shared__ int s_flag[kBinWarps][32];
-  __shared__ int s_src[kBinWarps][32];  // item-window position -> source lane
-  __shared__ float4 s_lv[kBinWarps][32];     // per lane: mx, my, first, seg0
-  __shared__ float4 s_gv[kBinWarps][32][2];  // per group: ellipse constants, rmin
-  stage_cams(s_cam);
-  __syncthreads();
-  constexpr int GPW = 32 / G;  // groups (records) per warp
-  const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
-  const bool lead = v == 0;
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
-  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
-       wb < n; wb += nwarps * GPW) {  // warp-uniform loop
-    const unsigned long long g = wb + gi;
-    const bool active = g < n;
-    uint32_t r = 0;
-    float4 m = make_float4(0.f, 0.f, 0.f, 1.f);
-    float4 q0 = make_float4(1.f, 1.f, 0.f, 1.f), q1 = make_float4(1.f, 0.f, 1.f, 0.f);
-    int k = 0;
-    if (active) {
-      r = recs[g];
-      k = (int)fdiv(r, c_fp.divM);
-      m = mean4[(long long)r - (long long)k * c_fp.M];
-      q0 = geom[2ull * r];
-      q1 = geom[2ull * r + 1];
-    }
-    const EllRec el = ell_load(q0, q1);
-    // ---- per view lane: exact mean (Eq.5) and AccuTile rows (O7)
-    const int j = k * s + v;
-    bool vis = false;
-    float mx = 0.f, my = 0.f;
-    int ty0 = 0x7fffffff, ty1 = -1;
-    if (active && v < s && j < N) {
-      const CamDev cam = load_cam(s_cam, j);
-      const F3 p = cam_point_exact(cam, m.x, m.y, m.z);
-      if (p.z >= c_fp.znear) {
-        mean2d_exact(cam, p, mx, my);
-        view_rows(el, my, TY, ty0, ty1);
-        vis = true;
-      }
-    }
-    const int rmin = max(gmin<G>(vis ? ty0 : 0x7fffffff), c_fp.row0);
-    const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
-    const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
-    // conservative reference column: every exact tx0 of the record is >= lo_ref
-    // unless rounding pushes a slice end past the ellipse extreme (then flagged)
-    const int xk = __float_as_int(mx);
-    const int kmin = gmin<G>(vis ? (xk ^ ((xk >> 31) & 0x7fffffff)) : 0x7f800000);
-    const float mxlo = __int_as_float(kmin ^ ((kmin >> 31) & 0x7fffffff));
-    const int lo_ref = (int)fmaxf(floorf((mxlo - el.ex - 15.5f) * 0.0625f) - 1.0f, -1.0f);
-    const bool fast = nrows > 0 && nrows <= kSlotRows;
-    int ni = 0, first = 0;
-    if (fast && vis) {
-      first = max(ty0, rmin);
-      ni = max(0, min(ty1, rmax) - first + 1);
-    }
-    if (lead) {
-      s_flag[w][gi] = 0;
-#pragma unroll
-      for (int t = 0; t < kSlotRows; ++t) s_mask[w][gi][t] = 0ull;
-    }
-    int pre = ni;  // warp inclusive prefix of (view,row) items
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, pre, 31);
-    const int seg0 = pre - ni;  // this lane's first item
-    s_lv[w][lane] = make_float4(mx, my, __int_as_float(first), __int_as_float(seg0));
-    if (lead) {
-      s_gv[w][gi][0] = make_float4(el.ex, el.ey, el.dyR, el.tc);
-      s_gv[w][gi][1] = make_float4(el.ic, el.b, el.det, __int_as_float(rmin));
-    }
-    __syncwarp();
-    // ---- (view, row) items, 32 per window: lane i takes item base+i
-    for (int base = 0; base < total; base += 32) {
-      // source lane of item base+lane: the lane whose item segment starts at the
-      // last segment start <= this window position (starts marked in s_src)
-      const bool inter = ni > 0 && pre > base && seg0 < base + 32;
-      const int spos = max(seg0, base) - base;
-      if (inter) s_src[w][spos] = lane;
-      const unsigned marks = __reduce_or_sync(0xffffffffu, inter ? (1u << spos) : 0u);
-      const int idx = base + lane;
-      const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-      const unsigned mk = marks & upto;
-      __syncwarp();
-      const int src = (idx < total && mk) ? s_src[w][31 - __clz(mk)] : 0;
-      // the source lane's / group's data from shared memory
-      const float4 lv = s_lv[w][src];
-      const float4 g0 = s_gv[w][src / G][0], g1 = s_gv[w][src / G][1];
-      const float smx = lv.x, smy = lv.y;
-      const int sfirst = __float_as_int(lv.z), sseg0 = __float_as_int(lv.w);
-      const int srmin = __float_as_int(g1.w);
-      const int slo = __shfl_sync(0xffffffffu, lo_ref, src);
-      EllRec e;
-      e.ex = g0.x; e.ey = g0.y; e.dyR = g0.z; e.tc = g0.w;
-      e.ic = g1.x; e.b = g1.y; e.det = g1.z;
-      if (idx < total) {
-        const int gs = src / G;
-        const int row = sfirst + (idx - sseg0);
-        int tx0, tx1;
-        if (view_row_cols(e, smx, smy, row, TX, tx0, tx1) && tx0 <= tx1) {
-          if (tx0 < slo || tx1 - slo >= 64) {
-            atomicOr(&s_flag[w][gs], 1);
-          } else {
-            const int len = tx1 - tx0 + 1;
-            const unsigned long long bits =
-                ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - slo);
-            // two native 32-bit shared ORs (a 64-bit OR would be a CAS loop)
-            unsigned* mw = reinterpret_cast<unsigned*>(&s_mask[w][gs][row - srmin]);
-            if ((unsigned)bits) atomicOr(mw, (unsigned)bits);
-            if ((unsigned)(bits >> 32)) atomicOr(mw + 1, (unsigned)(bits >> 32));
-          }
-        }
-      }
-    }
-    __syncwarp();
-    // ---- finalize fast records; general path for the rest
-    const bool slow = active && nrows > 0 && (!fast || s_flag[w][gi] != 0);
-    uint32_t c = 0;
-    const unsigned long long o = g;  // output index: list position
-    if (G >= 8) {  // the group's lanes write the slot (needs >= kSlotRows lanes)
-      // the group's lanes 0..3 each write one uint4 of the slot; lanes 0..5 count a row
-      const bool wr = active && fast && !slow;
-      uint32_t pc = (wr && v < kSlotRows) ? (uint32_t)__popcll(s_mask[w][gi][v]) : 0u;
-#pragma unroll
-      for (int q = 1; q < G; q <<= 1) pc += __shfl_xor_sync(0xffffffffu, pc, q);
-      if (wr) c = pc;
-      if (wr && v < 4) {
-        uint4 val;
-        if (v == 0) {
-          val = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
-        } else {
-          val = *reinterpret_cast<const uint4*>(&s_mask[w][gi][2 * (v - 1)]);
-        }
-        slots[4ull * o + v] = val;
-      }
-    } else if (active && fast && !slow && lead) {
-      unsigned long long mk[kSlotRows];
-#pragma unroll
-      for (int t = 0; t < kSlotRows; ++t) {
-        mk[t] = s_mask[w][gi][t];
-        c += (uint32_t)__popcll(mk[t]);
-      }
-      uint4* sl = slots + 4ull * o;
-      sl[0] = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
-      sl[1] = make_uint4((uint32_t)mk[0], (uint32_t)(mk[0] >> 32), (uint32_t)mk[1], (uint32_t)(mk[1] >> 32));
-      sl[2] = make_uint4((uint32_t)mk[2], (uint32_t)(mk[2] >> 32), (uint32_t)mk[3], (uint32_t)(mk[3] >> 32));
-      sl[3] = make_uint4((uint32_t)mk[4], (uint32_t)(mk[4] >> 32), (uint32_t)mk[5], (uint32_t)(mk[5] >> 32));
-    }
-    if (slow && lead) {  // footprint beyond the fast path: k_count_big
-      slots[4ull * o] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
-      big[atomicAdd(n_big, 1u)] = (uint32_t)o;
-    }
-    if (active && lead) cnt[o] = c;
-    __syncwarp();
-  }
-}
-
-// k_count2: as k_count, but every lane owns TWO views of its record (views
-// v*2 and v*2+1 of the cluster), so a G-lane group covers 2G views and a warp
-// takes 32/G records per step: the per-record share of loads, group
-// reductions, the item prefix scan and the slot write halves.  Same per-view
-// exact arithmetic, same union, same slot.
-template <int G>
-__global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restrict__ recs,
+// VPL = 2 (s >= 8): a G-lane group covers 2G views and a warp takes twice the
+// records per step, halving the per-record share of loads, group reductions,
+// the item prefix scan and the slot write (measured: binning 7.56 -> 6.58 ms
+// at config C; VPL = 4: 6.54 ms, not worth its 77 registers).
+template <int G, int VPL>
+__global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restrict__ recs,
                                                         uint32_t n,
                                                         const float4* __restrict__ mean4,
                                                         const float4* __restrict__ geom,
@@ -736,9 +554,9 @@ __global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restri
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
   __shared__ int s_src[kBinWarps][32];
-  __shared__ float4 s_lv[kBinWarps][32];     // per lane: view A mx, my, first; seg0
-  __shared__ float4 s_lv2[kBinWarps][32];    // per lane: view B mx, my, first; ni of A
-  __shared__ float4 s_gv[kBinWarps][32][2];  // per group: ellipse constants, rmin
+  __shared__ int s_seg[kBinWarps][32];            // per lane: first item of its segment
+  __shared__ float4 s_lv[kBinWarps][VPL][32];     // per lane, view u: mx, my, first, items before u
+  __shared__ float4 s_gv[kBinWarps][32][2];       // per group: ellipse constants, rmin
   stage_cams(s_cam);
   __syncthreads();
   constexpr int GPW = 32 / G;
@@ -762,13 +580,15 @@ __global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restri
       q1 = geom[2ull * r + 1];
     }
     const EllRec el = ell_load(q0, q1);
-    // ---- the lane's two views: exact means (Eq.5) and AccuTile rows (O7)
-    float mx[2] = {0.f, 0.f}, my[2] = {0.f, 0.f};
-    int ty0[2] = {0x7fffffff, 0x7fffffff}, ty1[2] = {-1, -1};
-    bool vis[2] = {false, false};
+    // ---- the lane's views: exact means (Eq.5) and AccuTile rows (O7)
+    float mx[VPL], my[VPL];
+    int ty0[VPL], ty1[VPL];
+    bool vis[VPL];
+    int tmin = 0x7fffffff, tmax = -1, kl = 0x7f800000;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int vv = 2 * v + u;
+    for (int u = 0; u < VPL; ++u) {
+      mx[u] = 0.f; my[u] = 0.f; ty0[u] = 0x7fffffff; ty1[u] = -1; vis[u] = false;
+      const int vv = VPL * v + u;
       const int j = k * s + vv;
       if (active && vv < s && j < N) {
         const CamDev cam = load_cam(s_cam, j);
@@ -777,31 +597,31 @@ __global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restri
           mean2d_exact(cam, p, mx[u], my[u]);
           view_rows(el, my[u], TY, ty0[u], ty1[u]);
           vis[u] = true;
+          tmin = min(tmin, ty0[u]);
+          tmax = max(tmax, ty1[u]);
+          const int xk = __float_as_int(mx[u]);
+          kl = min(kl, xk ^ ((xk >> 31) & 0x7fffffff));
         }
       }
     }
-    const int rmin = max(gmin<G>(min(vis[0] ? ty0[0] : 0x7fffffff, vis[1] ? ty0[1] : 0x7fffffff)),
-                         c_fp.row0);
-    const int rmax = min(gmax<G>(max(vis[0] ? ty1[0] : -1, vis[1] ? ty1[1] : -1)), c_fp.row1 - 1);
+    const int rmin = max(gmin<G>(tmin), c_fp.row0);
+    const int rmax = min(gmax<G>(tmax), c_fp.row1 - 1);
     const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
-    int kl = 0x7f800000;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int xk = __float_as_int(mx[u]);
-      if (vis[u]) kl = min(kl, xk ^ ((xk >> 31) & 0x7fffffff));
-    }
     const int kmin = gmin<G>(kl);
     const float mxlo = __int_as_float(kmin ^ ((kmin >> 31) & 0x7fffffff));
     const int lo_ref = (int)fmaxf(floorf((mxlo - el.ex - 15.5f) * 0.0625f) - 1.0f, -1.0f);
     const bool fast = nrows > 0 && nrows <= kSlotRows;
-    int nv[2] = {0, 0}, first[2] = {0, 0};
+    int ni = 0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < VPL; ++u) {
+      int f = 0, c = 0;
       if (fast && vis[u]) {
-        first[u] = max(ty0[u], rmin);
-        nv[u] = max(0, min(ty1[u], rmax) - first[u] + 1);
+        f = max(ty0[u], rmin);
+        c = max(0, min(ty1[u], rmax) - f + 1);
       }
-    const int ni = nv[0] + nv[1];
+      s_lv[w][u][lane] = make_float4(mx[u], my[u], __int_as_float(f), __int_as_float(ni));
+      ni += c;
+    }
     if (lead) {
       s_flag[w][gi] = 0;
 #pragma unroll
@@ -815,8 +635,7 @@ __global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restri
     }
     const int total = __shfl_sync(0xffffffffu, pre, 31);
     const int seg0 = pre - ni;
-    s_lv[w][lane] = make_float4(mx[0], my[0], __int_as_float(first[0]), __int_as_float(seg0));
-    s_lv2[w][lane] = make_float4(mx[1], my[1], __int_as_float(first[1]), __int_as_float(nv[0]));
+    s_seg[w][lane] = seg0;
     if (lead) {
       s_gv[w][gi][0] = make_float4(el.ex, el.ey, el.dyR, el.tc);
       s_gv[w][gi][1] = make_float4(el.ic, el.b, el.det, __int_as_float(rmin));
@@ -832,12 +651,16 @@ __global__ void __launch_bounds__(kBinThreads) k_count2(const uint32_t* __restri
       const unsigned mk = marks & upto;
       __syncwarp();
       const int src = (idx < total && mk) ? s_src[w][31 - __clz(mk)] : 0;
-      const float4 la = s_lv[w][src], lb = s_lv2[w][src];
-      const int loc = idx - __float_as_int(la.w);  // item index within the source lane
-      const bool inb = loc >= __float_as_int(lb.w);
-      const float smx = inb ? lb.x : la.x, smy = inb ? lb.y : la.y;
-      const int row = inb ? __float_as_int(lb.z) + (loc - __float_as_int(lb.w))
-                          : __float_as_int(la.z) + loc;
+      const int loc = idx - s_seg[w][src];  // item index within the source lane
+      // the source view: the last u whose items start at or before loc
+      float4 lv = s_lv[w][0][src];
+#pragma unroll
+      for (int u = 1; u < VPL; ++u) {
+        const float4 lu = s_lv[w][u][src];
+        if (loc >= __float_as_int(lu.w)) lv = lu;
+      }
+      const float smx = lv.x, smy = lv.y;
+      const int row = __float_as_int(lv.z) + (loc - __float_as_int(lv.w));
       const float4 g0 = s_gv[w][src / G][0], g1 = s_gv[w][src / G][1];
       const int srmin = __float_as_int(g1.w);
       const int slo = __shfl_sync(0xffffffffu, lo_ref, src);
