@@ -161,6 +161,17 @@ def cpu_model():
     return "unknown"
 
 
+def workload(cfg) -> str:
+    """The `config.workload` string both arms report for cfg."""
+    return (f"config {cfg.name}: {cfg.M} Gaussians SH{cfg.sh_degree} "
+            f"(scene_gen v1), {cfg.N}-view lenticular {cfg.W}x{cfg.H}")
+
+
+def scaling_of(cfg) -> str:
+    """Config E splits a fixed batch of poses per rank (weak); the others split one frame."""
+    return "weak" if cfg.name == "E" else "strong"
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -168,7 +179,9 @@ def run_reference(args, cfg):
     from paper_2605_04509_b200 import synthetic as sy  # noqa: F401
     scene, cams = cfg.make_scene(), cfg.make_rig()
     TY = (cfg.H + 15) // 16
-    rows = (TY // 2 - args.ref_rows // 2, TY // 2 - args.ref_rows // 2 + args.ref_rows)
+    nr = max(1, min(args.ref_rows, TY))
+    r0 = max(0, min(TY - nr, TY // 2 - nr // 2))
+    rows = (r0, r0 + nr)
     for _ in range(args.warmup):
         oracle_sample(cfg, scene, cams, rows)
     times = []
@@ -180,13 +193,13 @@ def run_reference(args, cfg):
     total = sum(times)
     value = args.steps * frac / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "metric": METRICS.get(cfg.name, METRIC), "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak" if pose_mode else "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"config {cfg.name}", "gaussians": cfg.M, "sh_degree": cfg.sh_degree,
-                   "views": cfg.N, "panel": f"{cfg.W}x{cfg.H}", "cluster_size": cfg.cluster_size,
+        "config": {"workload": workload(cfg), "cluster_size": cfg.cluster_size,
+                   "parallelism": "CPU oracle on the host cores (band sample)",
                    "sample_tile_rows": list(rows)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
                          "sample": last["sample"], "cpu": cpu_model()},
@@ -436,10 +449,9 @@ def main():
     line = {
         "metric": METRICS.get(cfg.name, METRIC), "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"config {cfg.name}: {cfg.M} Gaussians SH{cfg.sh_degree} "
-                               f"(scene_gen v1), {cfg.N}-view lenticular {cfg.W}x{cfg.H}",
+        "config": {"workload": workload(cfg),
                    "cluster_size": cfg.cluster_size, "remap": remap, "kernel": kernel,
                    "parallelism": (f"pose batch 256 split x{world}" if pose_mode else
                                    f"row-bands x{world} ({args.bands}: {bgt.bands or 'equal rows'})"
