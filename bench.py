@@ -135,9 +135,9 @@ def oracle_sample(cfg, scene, cams, rows, nthreads=0):
             "seconds": dt}
 
 
-def committed_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu table
-    (profiles/r*/ncu_kernels_configC.txt, written by tools/prof_all.sh)."""
+def committed_ncu(kernel: str):
+    """(DRAM bytes per launch, issued IPC per SM) of `kernel` from the newest
+    committed ncu table (profiles/r*/ncu_kernels_configC.txt, tools/prof_all.sh)."""
     import glob
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_kernels_configC.txt")),
                     reverse=True):
@@ -145,10 +145,11 @@ def committed_traffic(kernel: str):
             p = ln.split()
             if p and p[0].startswith(kernel) and len(p) >= 7:
                 try:  # columns: name.. n time_ms dram_GB GB/s IPC occ%
-                    return float(p[-4]) * 1e9 / int(p[-6]), os.path.relpath(f, ROOT)
+                    return (float(p[-4]) * 1e9 / int(p[-6]), float(p[-2]),
+                            os.path.relpath(f, ROOT))
                 except ValueError:
                     pass
-    return None, None
+    return None, None, None
 
 
 def cpu_model():
@@ -439,7 +440,7 @@ def main():
     achieved_tflops = evals * FLOPS_PER_EVAL / (comp_ms * 1e-3) / 1e12 if comp_ms > 0 else None
     peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     bc = compulsory_bytes(cfg, info) if world == 1 else None
-    traffic, traffic_src = committed_traffic("k_composite_staged")
+    traffic, ipc, traffic_src = committed_ncu("k_composite_staged")
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rows_s = (TY // 2 - args.ref_rows // 2, TY // 2 - args.ref_rows // 2 + args.ref_rows)
@@ -465,6 +466,9 @@ def main():
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
                      "traffic": traffic, "traffic_source": traffic_src,
+                     # the kernel is instruction-issue bound: issued IPC per SM of the
+                     # 4 schedulers (ncu sm__inst_executed.avg.per_cycle_active)
+                     "issue_ipc": ipc, "issue_frac": (ipc / 4.0) if ipc else None,
                      "note": (f"{FLOPS_PER_EVAL} algorithmic FP32 ops per (subpixel, splat) "
                               f"evaluation x {evals} evaluations / mean composite time; peak = "
                               f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §5)")},
