@@ -8,7 +8,7 @@
 //   onesweep x4 (k, depth)      a7 depth presort of the records              HBM/issue
 //   count + count_big           a6 cluster tile unions, list-position order  ALU
 //   scan(counts)                pair offsets, P                              HBM
-//   emit_flat + emit_big        a6 <tile, r> pairs in (k, depth, i) order    HBM
+//   emit_rows + emit_big        a6 <tile, r> pairs in (k, depth, i) order    HBM
 //   hist + onesweep x2..3       a7 stable tile sort                          HBM/issue
 //   ranges                      a8                                           HBM
 //   composite                   a9                                           ALU/MUFU
@@ -809,10 +809,10 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
   if (P > 0) {
     // big-footprint records are emitted on a forked stream, concurrently with
-    // k_emit_flat (disjoint output positions); joined before the tile sort
+    // k_emit_rows (disjoint output positions); joined before the tile sort
     CR_CUDA(c, cudaEventRecord(c->ev_fork, str));
     CR_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    k_emit_flat<<<(unsigned)std::min<long long>((nvis + 255) / 256, 148 * 16), 256, 0, str>>>(
+    k_emit_rows<<<(unsigned)std::min<long long>((nvis + 255) / 256, 148 * 16), 256, 0, str>>>(
         rec_sorted, P_<uint32_t>(c->offs), nvis, P, P_<uint4>(c->slots), tA, pA);
     CR_LAUNCHED(c);
 #define CR_EMITB(GG)                                                                        \
