@@ -19,6 +19,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -666,6 +667,73 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
                                      cudaMemcpyHostToDevice, str));
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_rep, rep.data(), sizeof(int) * K, 0,
                                      cudaMemcpyHostToDevice, str));
+  {  // cluster motion bounds for the band / frame pre-cull (fp64, rounded up)
+    std::vector<float4> clb(K);
+    std::vector<float> cldb(K);
+    for (int k = 0; k < K; ++k) {
+      const CamDev& cr = c->cams[rep[k]];
+      std::vector<std::array<double, 12>> mv;  // (A - I) row-major, then b
+      for (int j = k * s; j < std::min(k * s + s, N); ++j) {
+        const CamDev& cj = c->cams[j];
+        std::array<double, 12> q{};
+        for (int a = 0; a < 3; ++a)
+          for (int bb = 0; bb < 3; ++bb) {  // A = R_j R_rep^T
+            double v = 0.0;
+            for (int z = 0; z < 3; ++z) v += (double)cj.R[a * 3 + z] * (double)cr.R[bb * 3 + z];
+            q[a * 3 + bb] = v;
+          }
+        for (int a = 0; a < 3; ++a) {  // b = t_j - A t_rep
+          double v = (double)cj.t[a];
+          for (int z = 0; z < 3; ++z) v -= q[a * 3 + z] * (double)cr.t[z];
+          q[9 + a] = v;
+        }
+        for (int a = 0; a < 3; ++a) q[a * 3 + a] -= 1.0;
+        mv.push_back(q);
+      }
+      // centre: argmin_c sum_j |(A_j - I) c + b_j|^2, lightly regularised (Cramer)
+      double Mm[9] = {0}, rhs[3] = {0};
+      for (const auto& q : mv)
+        for (int a = 0; a < 3; ++a) {
+          for (int bb = 0; bb < 3; ++bb)
+            for (int z = 0; z < 3; ++z) Mm[a * 3 + bb] += q[z * 3 + a] * q[z * 3 + bb];
+          for (int z = 0; z < 3; ++z) rhs[a] -= q[z * 3 + a] * q[9 + z];
+        }
+      const double tr = Mm[0] + Mm[4] + Mm[8];
+      for (int a = 0; a < 3; ++a) Mm[a * 3 + a] += 1e-9 * tr + 1e-300;
+      auto det3 = [](const double* m) {
+        return m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+               m[2] * (m[3] * m[7] - m[4] * m[6]);
+      };
+      double cc[3] = {0, 0, 0};
+      const double dM = det3(Mm);
+      if (std::isfinite(dM) && dM != 0.0)
+        for (int a = 0; a < 3; ++a) {
+          double t3[9];
+          std::memcpy(t3, Mm, sizeof(t3));
+          for (int z = 0; z < 3; ++z) t3[z * 3 + a] = rhs[z];
+          cc[a] = det3(t3) / dM;
+          if (!std::isfinite(cc[a])) cc[a] = 0.0;
+        }
+      double dA = 0.0, db = 0.0;  // the bound holds for ANY c; the centre only tightens it
+      for (const auto& q : mv) {
+        double fro = 0.0, b2 = 0.0;
+        for (int a = 0; a < 9; ++a) fro += q[a] * q[a];
+        for (int a = 0; a < 3; ++a) {
+          double v = q[9 + a];
+          for (int z = 0; z < 3; ++z) v += q[a * 3 + z] * cc[z];
+          b2 += v * v;
+        }
+        dA = std::max(dA, std::sqrt(fro));
+        db = std::max(db, std::sqrt(b2));
+      }
+      clb[k] = make_float4((float)cc[0], (float)cc[1], (float)cc[2], (float)(dA * 1.0001 + 1e-7));
+      cldb[k] = (float)(db * 1.0001 + 1e-6);
+    }
+    CR_CUDA(c, cudaMemcpyToSymbolAsync(c_clb, clb.data(), sizeof(float4) * K, 0,
+                                       cudaMemcpyHostToDevice, str));
+    CR_CUDA(c, cudaMemcpyToSymbolAsync(c_cldb, cldb.data(), sizeof(float) * K, 0,
+                                       cudaMemcpyHostToDevice, str));
+  }
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_fp, &fp, sizeof(fp), 0, cudaMemcpyHostToDevice, str));
 
   // ---- composite work items (static per display and s)

@@ -61,6 +61,13 @@ struct FrameParams {
 __constant__ CamDev c_cams[kMaxViews];
 __constant__ CamConstDev c_ccon[kMaxViews];
 __constant__ int c_rep[kMaxViews];
+// Per cluster k: bound of the camera-space displacement between the
+// representative view and any view j of the cluster.  With p_j = A_j p + b_j
+// (p in rep camera space) and a centre c (least-squares fixed point of the
+// cluster's rigid motions): |p_j - p| <= dA |p - c| + db, dA = max_j ||A_j - I||_F,
+// db = max_j |(A_j - I) c + b_j|.  c_clb[k] = (c.x, c.y, c.z, dA), c_cldb[k] = db.
+__constant__ float4 c_clb[kMaxViews];
+__constant__ float c_cldb[kMaxViews];
 __constant__ FrameParams c_fp;
 
 // ---------------------------------------------------------------- exact ops
