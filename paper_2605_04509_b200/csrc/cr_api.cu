@@ -138,6 +138,7 @@ struct cr_ctx {
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
   int exp = 0;         // CR_EXP: kernel-variant A/B experiments (read per render)
+  bool motion_bound = false;  // pre-cull by the cluster motion bound (narrow clusters)
 };
 
 namespace {
@@ -670,6 +671,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   {  // cluster motion bounds for the band / frame pre-cull (fp64, rounded up)
     std::vector<float4> clb(K);
     std::vector<float> cldb(K);
+    double maxdA = 0.0;
     for (int k = 0; k < K; ++k) {
       const CamDev& cr = c->cams[rep[k]];
       std::vector<std::array<double, 12>> mv;  // (A - I) row-major, then b
@@ -727,12 +729,14 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
         db = std::max(db, std::sqrt(b2));
       }
       clb[k] = make_float4((float)cc[0], (float)cc[1], (float)cc[2], (float)(dA * 1.0001 + 1e-7));
+      maxdA = std::max(maxdA, dA);
       cldb[k] = (float)(db * 1.0001 + 1e-6);
     }
     CR_CUDA(c, cudaMemcpyToSymbolAsync(c_clb, clb.data(), sizeof(float4) * K, 0,
                                        cudaMemcpyHostToDevice, str));
     CR_CUDA(c, cudaMemcpyToSymbolAsync(c_cldb, cldb.data(), sizeof(float) * K, 0,
                                        cudaMemcpyHostToDevice, str));
+    c->motion_bound = maxdA < (double)kMotionBoundMax;  // narrow clusters: one projection
   }
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_fp, &fp, sizeof(fp), 0, cudaMemcpyHostToDevice, str));
 
@@ -783,7 +787,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (M > 0) {
     const unsigned g = grid_for(M, 128);
 #define CR_PRE(D)                                                                               \
-  k_preprocess<D><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
+  if (c->motion_bound) CR_PRE2(D, true); else CR_PRE2(D, false)
+#define CR_PRE2(D, MBV)                                                                         \
+  k_preprocess<D, MBV><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
                                       P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
                                       P_<float4>(c->rec0) + 1, P_<float4>(c->geom),                 \
                                       P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters, sc + 16)
@@ -794,6 +800,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       default: CR_PRE(3); break;
     }
 #undef CR_PRE
+#undef CR_PRE2
     CR_LAUNCHED(c);
     CR_TRACE(c, "preprocess");
     // visible (i,k) records straight to presort (key, r) pairs, (k, i) order

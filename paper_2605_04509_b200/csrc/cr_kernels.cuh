@@ -370,6 +370,44 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
 // ===========================================================================
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Per-view variant of the pre-cull (clusters spanning wide camera motions,
+// where the rigid-motion bound below is loose): with
+// fast FMA math and a rigorous padding for its rounding (|p_fast - p_exact| <=
+// ~1e-6 (|mu|_1 + |t|_1) per coordinate), decide whether ANY view of cluster
+// k could give the record a tile in the band rows x frame columns.  When this
+// returns false the exact union (O8) is empty, so skipping the record changes
+// no result; when in doubt (near-znear depths) it returns true.
+__device__ __forceinline__ bool may_touch_band_views(int k, float mx, float my, float mz, float exw,
+                                               float eyw) {
+  const int s = c_fp.s, N = c_fp.N;
+  const int j0 = k * s, j1 = min(j0 + s, N);
+  const float S = fabsf(mx) + fabsf(my) + fabsf(mz);
+  const float ylo = 16.0f * (float)c_fp.row0 - 16.0f, yhi = 16.0f * (float)c_fp.row1 + 16.0f;
+  const float xlo = -16.0f, xhi = 16.0f * (float)c_fp.TX + 16.0f;
+  bool hit = false;
+  for (int j = j0; j < j1; ++j) {  // j is warp-uniform (one k per launch-wide loop step)
+    const CamDev& c = c_cams[j];
+    const float px = fmaf(c.R[0], mx, fmaf(c.R[1], my, fmaf(c.R[2], mz, c.t[0])));
+    const float py = fmaf(c.R[3], mx, fmaf(c.R[4], my, fmaf(c.R[5], mz, c.t[1])));
+    const float pz = fmaf(c.R[6], mx, fmaf(c.R[7], my, fmaf(c.R[8], mz, c.t[2])));
+    const float err = 4e-6f * (S + fabsf(c.t[0]) + fabsf(c.t[1]) + fabsf(c.t[2]) + 1.0f);
+    if (pz + err < c_fp.znear) continue;        // certainly invisible from view j
+    if (pz < 2.0f * c_fp.znear + err) {         // too close to call
+      hit = true;
+      continue;
+    }
+    const float iz = __fdividef(1.0f, pz);  // approximate: covered by the padding
+    const float u = px * iz, v = py * iz;
+    const float ex = c.fx * u + c.cx, ey = c.fy * v + c.cy;
+    const float mgx = c.fx * err * iz * (1.0f + fabsf(u)) * 2.0f + 1e-5f * fabsf(ex) + 1.0f;
+    const float mgy = c.fy * err * iz * (1.0f + fabsf(v)) * 2.0f + 1e-5f * fabsf(ey) + 1.0f;
+    const bool in = ey + eyw + mgy >= ylo && ey - eyw - mgy <= yhi && ex + exw + mgx >= xlo &&
+                    ex - exw - mgx <= xhi;
+    hit |= in;  // no early exit: the warp stays converged over the cluster's views
+  }
+  return hit;
+}
+
 // Conservative band / frame pre-cull of an (i,k) record (exactness-safe).
 // Only the representative view is projected, from the record's exact
 // camera-space point p: every view j of cluster k sees p_j = A_j p + b_j, and
@@ -380,8 +418,11 @@ constexpr float kLog2e = 1.4426950408889634f;
 // rounding: 1 %, 2e-5 relative, 3 px) misses the band rows x frame columns, no
 // view can give the record a tile there: the exact union (O8) is empty and
 // skipping the record changes no result.  Near-znear depths return true.
-// (Replaced a per-view projection loop over the cluster: preprocess 1.78 ->
-// 1.03 ms at config C for 5 % more surviving records, all with empty unions.)
+// Used when every cluster's rotation bound dA < kMotionBoundMax (narrow
+// clusters, e.g. config C: preprocess 1.78 -> 1.02 ms for 5 % more surviving
+// records, all with empty unions); wider clusters (B, E, P2K, P4K) keep the
+// per-view test, where the bound would let through up to 27 % more records.
+constexpr float kMotionBoundMax = 0.08f;
 __device__ __forceinline__ bool may_touch_band(int k, int jr, const F3& p, float exw,
                                                float eyw) {
   const float ylo = 16.0f * (float)c_fp.row0 - 16.0f, yhi = 16.0f * (float)c_fp.row1 + 16.0f;
@@ -402,7 +443,7 @@ __device__ __forceinline__ bool may_touch_band(int k, int jr, const F3& p, float
          ex - exw - sx <= xhi;
 }
 
-template <int DEG>
+template <int DEG, bool MB>
 __global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
     const float* __restrict__ shsoa, float4* __restrict__ rec0, float4* __restrict__ rec1,
@@ -442,7 +483,9 @@ __global__ void __launch_bounds__(128) k_preprocess(
         dkey[r] = __float_as_uint(p.z);
         {  // exact per-record AccuTile constants (O7), used by count and emit
           const EllRec el = ell_rec(a, b, c, det, tau);
-          if (!may_touch_band(k, jr, p, el.ex * 1.001f + 1.0f, el.ey * 1.001f + 1.0f)) {
+          if (MB ? !may_touch_band(k, jr, p, el.ex * 1.001f + 1.0f, el.ey * 1.001f + 1.0f)
+                 : !may_touch_band_views(k, m.x, m.y, m.z, el.ex * 1.001f + 1.0f,
+                                         el.ey * 1.001f + 1.0f)) {
             vis[r] = 0;  // no view can reach the band / frame: empty union
             continue;
           }
