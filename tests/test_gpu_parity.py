@@ -383,3 +383,19 @@ def test_big_footprints_general_path():
         g.render(cluster_size=s, stats=True)
         assert g.last_stats["emit_fallback"] > 0, "general path not exercised"
     check_frame(g, o, 4, rows=(1, 5))
+
+
+def test_parallel_camera_rig_motion_bound():
+    """A camera-array rig (pure translation between views, no rotation): every
+    cluster's rotation bound is 0, so the pre-cull takes the rigid-motion-bound
+    path (one projection per record); the result must still be bit-exact,
+    full frame and in a band."""
+    _need_gpu()
+    W, H, N = 256, 144, 16
+    sc = sy.random_scene(4000, 1, seed=17, scale_median=0.03)
+    cams = sy.identical_rig(N, W, H, radius=3.0, height=0.3, fov_y_deg=50.0).copy()
+    cams[:, 9] += np.linspace(-0.12, 0.12, N, dtype=np.float32)  # camera-space x offsets
+    g, o = make_pair(sc, W, H, N, 11.3, 0.19, 1.7, cams)
+    for s in (4, 8):
+        check_frame(g, o, s)
+    check_frame(g, o, 8, rows=(3, 6))
