@@ -399,3 +399,25 @@ def test_parallel_camera_rig_motion_bound():
     for s in (4, 8):
         check_frame(g, o, s)
     check_frame(g, o, 8, rows=(3, 6))
+
+
+def test_wide_depth_range_uncompressed_presort():
+    """Depths spanning 0.05 .. 1e9 with K = 16 clusters: the compressed
+    (k, depth - min) presort key needs more than 32 bits, so the presort falls
+    back to a 32-bit depth sort plus a stable cluster pass; still bit-exact."""
+    _need_gpu()
+    W, H, N = 192, 112, 16
+    rng = np.random.default_rng(23)
+    n = 3000
+    sc = sy.random_scene(n, 0, seed=23, scale_median=0.03)
+    cams = sy.orbit_rig(N, 12.0, W, H, radius=3.0, height=0.0, fov_y_deg=50.0)
+    # spread the Gaussians along the rig's viewing direction, log-uniform in depth
+    zc = np.exp(rng.uniform(np.log(0.05), np.log(1e9), n))
+    dirs = sc["means"] / np.maximum(np.linalg.norm(sc["means"], axis=1, keepdims=True), 1e-6)
+    eye = np.array([0.0, 0.0, 3.0])
+    means = eye[None, :] + (np.array([0.0, 0.0, -1.0])[None, :] + 0.3 * dirs) * zc[:, None]
+    sc["means"] = means.astype(np.float32)
+    sc["scales"] = (sc["scales"] * np.maximum(zc, 1.0)[:, None] * 0.3).astype(np.float32)
+    g, o = make_pair(sc, W, H, N, 9.9, 0.21, 0.4, cams)
+    check_frame(g, o, 1)
+    check_frame(g, o, 2)
