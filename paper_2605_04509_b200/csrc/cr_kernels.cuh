@@ -1,11 +1,11 @@
-// cr_kernels.cuh — display, upload, preprocess (+tile-union count), emit and
-// range kernels of the CoherentRaster B200 path.  See DESIGN.md §5 for the
+// cr_kernels.cuh — display (view map, Ψ, composite work items), upload,
+// preprocess, tile-union count, emission and range kernels of the
+// CoherentRaster B200 path.  See DESIGN.md §5 for the
 // roofline of each kernel and its algorithmic bytes per unit.
 #pragma once
 #include <cuda_fp16.h>
 
 #include "cr_device.cuh"
-#include "cr_sort.cuh"
 
 namespace cr {
 
@@ -888,7 +888,6 @@ __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __res
 }
 
 constexpr int kMaxRows = 288;  // >= TY for 8K (270 tile rows)
-constexpr int kMaxRowsBin = kMaxRows;
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
