@@ -295,7 +295,7 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
 constexpr int kOneItems = 16;
 cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uint32_t*& vB,
                      long long n, int shift0, int npass, unsigned aggmask = 0,
-                     bool hist_ready = false) {
+                     bool hist_ready = false, uint32_t slotK = 0) {
   if (n <= 0 || npass <= 0) return CR_OK;
   if (npass > 4) return fail(c, CR_ERR_CAPACITY, "radix_sort: npass %d > 4", npass);
   constexpr long long kTile = (long long)kSortThreads * kOneItems;
@@ -327,7 +327,7 @@ cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uin
     }
     k_radix_onesweep<kOneItems><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
         kA, vA, kB, vB, n, shift0 + 8 * p, gh + 256 * p, P_<unsigned long long>(c->look),
-        ctr + p, c->epoch);
+        ctr + p, c->epoch, p == npass - 1 ? slotK : 0u);
     CR_LAUNCHED(c);
     std::swap(kA, kB);
     std::swap(vA, vB);
@@ -916,7 +916,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     unsigned agg = 0;
     for (int sh = 8, q = 1; sh < tbits; sh += 8, ++q)
       if (((long long)(row1 - row0) * TX >> sh) < 64) agg |= 1u << q;
-    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, tpass, agg));
+    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, tpass, agg, false, (uint32_t)K));
   }
   const size_t nSE = (size_t)TX * TY * K;
   CR_TRY(ensure(c, c->S, nSE * 4));
@@ -925,7 +925,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_CUDA(c, cudaMemsetAsync(c->E.p, 0, nSE * 4, str));
   if (P > 0) {
     k_ranges<<<(unsigned)std::min<long long>(grid_for((P + 3) / 4, 256), 148 * 8), 256, 0, str>>>(
-        tA, pA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
+        tA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
     CR_LAUNCHED(c);
   }
   CR_TRACE(c, "tile sort+ranges");

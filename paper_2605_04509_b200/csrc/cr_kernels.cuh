@@ -968,35 +968,31 @@ __global__ void k_pair_counts(const uint32_t* __restrict__ val, uint32_t P,
 
 // ===========================================================================
 // a8 — ranges [S_{t,k}, E_{t,k}) from the (t, k)-sorted pairs.
+// slot[e] = t*K + k, written by the tile sort's last pass (k_radix_onesweep
+// with slotK = K), so only the keys are read.
 // ===========================================================================
-__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ tkey,
-                                                const uint32_t* __restrict__ val, uint32_t P,
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ slot, uint32_t P,
                                                 uint32_t* __restrict__ S, uint32_t* __restrict__ E) {
   // 4 consecutive pairs per thread (16-byte loads), grid-stride over quads;
-  // (t, k) slot keys of the neighbours via shuffles, lanes 0/31 load their
-  // outer neighbour once.  Buffers are padded, so a partial last quad is safe.
+  // neighbour slots via shuffles, lanes 0/31 load their outer neighbour once.
+  // Buffers are padded, so a partial last quad is safe.
   const int lane = threadIdx.x & 31;
-  const uint32_t K = (uint32_t)c_fp.K;
   const uint32_t nq = (P + 3) / 4;
-  auto slot_of = [&](uint32_t e) -> uint32_t {
-    return tkey[e] * K + fdiv(val[e], c_fp.divM);
-  };
   for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < nq; q0 += gridDim.x * blockDim.x) {
     const uint32_t q = q0 + threadIdx.x;
     const uint32_t e = 4 * q;
     uint32_t key[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
     if (q < nq) {
-      const uint4 tt = reinterpret_cast<const uint4*>(tkey)[q];
-      const uint4 vv = reinterpret_cast<const uint4*>(val)[q];
-      const uint32_t ta[4] = {tt.x, tt.y, tt.z, tt.w}, va[4] = {vv.x, vv.y, vv.z, vv.w};
+      const uint4 tt = reinterpret_cast<const uint4*>(slot)[q];
+      const uint32_t ta[4] = {tt.x, tt.y, tt.z, tt.w};
 #pragma unroll
       for (int h = 0; h < 4; ++h)
-        if (e + h < P) key[h] = ta[h] * K + fdiv(va[h], c_fp.divM);
+        if (e + h < P) key[h] = ta[h];
     }
     uint32_t prev = __shfl_up_sync(0xffffffffu, key[3], 1);
     uint32_t next = __shfl_down_sync(0xffffffffu, key[0], 1);
-    if (lane == 0) prev = (q < nq && e > 0) ? slot_of(e - 1) : 0xFFFFFFFEu;
-    if (lane == 31) next = (q < nq && e + 4 < P) ? slot_of(e + 4) : 0xFFFFFFFEu;
+    if (lane == 0) prev = (q < nq && e > 0) ? slot[e - 1] : 0xFFFFFFFEu;
+    if (lane == 31) next = (q < nq && e + 4 < P) ? slot[e + 4] : 0xFFFFFFFEu;
     if (q >= nq) continue;
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -1011,7 +1007,8 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ tke
 }
 
 // Introspection: 64-bit keys of Eq.11 and payload i.
-__global__ void k_make_keys(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ val,
+// slot[e] = t*K + k (the tile sort's output, see k_ranges).
+__global__ void k_make_keys(const uint32_t* __restrict__ slot, const uint32_t* __restrict__ val,
                             const uint32_t* __restrict__ dkey, uint32_t P,
                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ pay) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1019,7 +1016,8 @@ __global__ void k_make_keys(const uint32_t* __restrict__ tkey, const uint32_t* _
   const unsigned long long M = (unsigned long long)c_fp.M;
   const uint32_t r = val[e];
   const unsigned long long k = fdiv(r, c_fp.divM);
-  keys[e] = ((unsigned long long)tkey[e] << (32 + c_fp.bitK)) | (k << 32) |
+  const unsigned long long t = slot[e] / (uint32_t)c_fp.K;
+  keys[e] = (t << (32 + c_fp.bitK)) | (k << 32) |
             (unsigned long long)dkey[r];
   pay[e] = (uint32_t)(r - k * M);
 }

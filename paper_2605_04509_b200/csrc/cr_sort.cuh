@@ -441,6 +441,8 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
 
 // one stable pass on digit (key >> shift) & 255; ghist = this digit's global
 // histogram; look = [tiles][256] status words; ctr = tile counter (zeroed).
+// slotK != 0 (last tile-sort pass only): write the (t, k) range slot
+// t*K + k (k = val / M) instead of the key t, so k_ranges reads keys only.
 // Ranks by 8-ballot multisplit peers (measured faster than match.any.sync on
 // B200: 4.37 vs 4.88 ms for the frame's 6 passes; 16 items/thread beat 12).
 template <int ITEMS>
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
     const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ look,
-    uint32_t* __restrict__ ctr, uint32_t epoch) {
+    uint32_t* __restrict__ ctr, uint32_t epoch, uint32_t slotK) {
   constexpr int TILE = kSortThreads * ITEMS;
   __shared__ uint32_t s_cnt[kSortWarps][256];  // counts -> block-local warp offsets
   __shared__ uint32_t s_off[256];              // global base - block-local offset
@@ -535,10 +537,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   __syncthreads();
   const int cnt = (int)min((long long)TILE, n - bbase);
   for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
-    const uint32_t k = s_k[p];
+    const uint32_t k = s_k[p], v = s_v[p];
     const uint32_t gp = s_off[(k >> shift) & 255u] + (uint32_t)p;
-    vals_out[gp] = s_v[p];
-    keys_out[gp] = k;
+    vals_out[gp] = v;
+    keys_out[gp] = slotK ? k * slotK + fdiv(v, c_fp.divM) : k;
   }
 }
 
