@@ -445,13 +445,42 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
 // t*K + k (k = val / M) instead of the key t, so k_ranges reads keys only.
 // Ranks by 8-ballot multisplit peers (measured faster than match.any.sync on
 // B200: 4.37 vs 4.88 ms for the frame's 6 passes; 16 items/thread beat 12).
-template <int ITEMS>
+// VAR bit 0: full tiles skip the bounds checks; bit 1: scatter into shared
+// memory before the look-back (the wait overlaps the local scatter).
+template <int ITEMS, bool FULL>
+__device__ __forceinline__ void onesweep_rank(const uint32_t* __restrict__ keys,
+                                              const uint32_t* __restrict__ vals, long long n,
+                                              long long wbase, int shift, int lane, unsigned lt,
+                                              uint32_t* s_cw, uint32_t* kr, uint32_t* vr,
+                                              uint32_t* dl) {
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const long long e = wbase + q * 32 + lane;
+    const bool ok = FULL || e < n;
+    kr[q] = ok ? keys[e] : 0u;
+    vr[q] = ok ? vals[e] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const bool ok = FULL || wbase + q * 32 + lane < n;
+    const uint32_t d = ok ? ((kr[q] >> shift) & 255u) : 256u;
+    const unsigned peers = FULL ? warp_peers8(d, true) : warp_peers8(d, ok);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (ok && lane == leader) old = atomicAdd(&s_cw[d], (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
+    dl[q] = d | ((old + __popc(peers & lt)) << 9);
+  }
+}
+
+template <int ITEMS, int VAR>
 __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
     const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ look,
     uint32_t* __restrict__ ctr, uint32_t epoch, uint32_t slotK) {
   constexpr int TILE = kSortThreads * ITEMS;
+  constexpr bool LATE = (VAR & 2) != 0;
   __shared__ uint32_t s_cnt[kSortWarps][256];  // counts -> block-local warp offsets
   __shared__ uint32_t s_off[256];              // global base - block-local offset
   __shared__ uint32_t s_k[TILE];
@@ -467,24 +496,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   const long long bbase = (long long)bid * TILE;
   const long long wbase = bbase + (long long)w * (ITEMS * 32);
   uint32_t kr[ITEMS], vr[ITEMS], dl[ITEMS];  // dl = digit | rank << 9
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const long long e = wbase + q * 32 + lane;
-    const bool ok = e < n;
-    kr[q] = ok ? keys[e] : 0u;
-    vr[q] = ok ? vals[e] : 0u;
-  }
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const bool ok = wbase + q * 32 + lane < n;
-    const uint32_t d = ok ? ((kr[q] >> shift) & 255u) : 256u;
-    const unsigned peers = warp_peers8(d, ok);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (ok && lane == leader) old = atomicAdd(&s_cnt[w][d], (uint32_t)__popc(peers));
-    old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
-    dl[q] = d | ((old + __popc(peers & lt)) << 9);
-  }
+  if ((VAR & 1) && bbase + TILE <= n)
+    onesweep_rank<ITEMS, true>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
+  else
+    onesweep_rank<ITEMS, false>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
   __syncthreads();
   const int d = threadIdx.x;  // kSortThreads == 256: one digit per thread
   uint32_t acc = 0;
@@ -511,7 +526,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   if (lane == 31) { s_ws[0][w] = i1; s_ws[1][w] = i2; }
   // look back for the exclusive prefix of digit d over the preceding tiles
   uint32_t excl = 0;
-  if (bid > 0) {
+  if (!LATE && bid > 0) {
     excl = lookback4(look + (size_t)(bid - 1) * 256 + d, (long long)bid, 256, epoch);
     st_status(my, hiP | (excl + acc));
   }
@@ -521,7 +536,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   for (int ww = 0; ww < kSortWarps; ++ww)
     if (ww < w) { p1 += s_ws[0][ww]; p2 += s_ws[1][ww]; }
   const uint32_t loff = p1 + i1 - acc;
-  s_off[d] = (p2 + i2 - gh) + excl - loff;
+  if (!LATE) s_off[d] = (p2 + i2 - gh) + excl - loff;
 #pragma unroll
   for (int ww = 0; ww < kSortWarps; ++ww) s_cnt[ww][d] += loff;
   __syncthreads();
@@ -533,6 +548,13 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
       s_v[p] = vr[q];
       s_k[p] = kr[q];
     }
+  }
+  if (LATE) {
+    if (bid > 0) {
+      excl = lookback4(look + (size_t)(bid - 1) * 256 + d, (long long)bid, 256, epoch);
+      st_status(my, hiP | (excl + acc));
+    }
+    s_off[d] = (p2 + i2 - gh) + excl - loff;
   }
   __syncthreads();
   const int cnt = (int)min((long long)TILE, n - bbase);
