@@ -325,10 +325,7 @@ cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uin
       CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
       c->epoch = 1;
     }
-    // full tiles without bounds checks, look-back after the shared-memory
-    // scatter (measured at config C: sort 4.26 -> 3.64 ms; either alone 3.94 /
-    // 4.11 ms)
-    k_radix_onesweep<kOneItems, 3><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+    k_radix_onesweep<kOneItems, 7, 5><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
         kA, vA, kB, vB, n, shift0 + 8 * p, gh + 256 * p, P_<unsigned long long>(c->look),
         ctr + p, c->epoch, p == npass - 1 ? slotK : 0u);
     CR_LAUNCHED(c);

@@ -446,8 +446,13 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
 // Ranks by 8-ballot multisplit peers (measured faster than match.any.sync on
 // B200: 4.37 vs 4.88 ms for the frame's 6 passes; 16 items/thread beat 12).
 // VAR bit 0: full tiles skip the bounds checks; bit 1: scatter into shared
-// memory before the look-back (the wait overlaps the local scatter).
-template <int ITEMS, bool FULL>
+// memory before the look-back (the wait overlaps the local scatter); bit 2:
+// values loaded at the scatter, not held in registers through the ranking.
+// Shipped: VAR = 7 at 5 CTAs/SM (measured at config C, sort stage: 4.26 ms
+// for VAR = 0 at 3 CTAs/SM; 3.94 bit 0; 4.11 bit 1; 3.64 bits 0+1; 3.55 bits
+// 0+1 at 4 CTAs/SM; 3.40 VAR = 7 at 5 CTAs/SM; 12 items at 6 CTAs/SM and
+// keys re-read at the scatter were slower).
+template <int ITEMS, bool FULL, bool VALS>
 __device__ __forceinline__ void onesweep_rank(const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals, long long n,
                                               long long wbase, int shift, int lane, unsigned lt,
@@ -458,7 +463,7 @@ __device__ __forceinline__ void onesweep_rank(const uint32_t* __restrict__ keys,
     const long long e = wbase + q * 32 + lane;
     const bool ok = FULL || e < n;
     kr[q] = ok ? keys[e] : 0u;
-    vr[q] = ok ? vals[e] : 0u;
+    if (VALS) vr[q] = ok ? vals[e] : 0u;
   }
 #pragma unroll
   for (int q = 0; q < ITEMS; ++q) {
@@ -473,8 +478,8 @@ __device__ __forceinline__ void onesweep_rank(const uint32_t* __restrict__ keys,
   }
 }
 
-template <int ITEMS, int VAR>
-__global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
+template <int ITEMS, int VAR, int MINB = 3>
+__global__ void __launch_bounds__(kSortThreads, MINB) k_radix_onesweep(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
     const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ look,
@@ -496,10 +501,11 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
   const long long bbase = (long long)bid * TILE;
   const long long wbase = bbase + (long long)w * (ITEMS * 32);
   uint32_t kr[ITEMS], vr[ITEMS], dl[ITEMS];  // dl = digit | rank << 9
+  constexpr bool VALS = (VAR & 4) == 0;  // bit 2: values loaded at the scatter
   if ((VAR & 1) && bbase + TILE <= n)
-    onesweep_rank<ITEMS, true>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
+    onesweep_rank<ITEMS, true, VALS>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
   else
-    onesweep_rank<ITEMS, false>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
+    onesweep_rank<ITEMS, false, VALS>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
   __syncthreads();
   const int d = threadIdx.x;  // kSortThreads == 256: one digit per thread
   uint32_t acc = 0;
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_radix_onesweep(
     const uint32_t dq = dl[q] & 511u;
     if (dq < 256) {
       const uint32_t p = s_cnt[w][dq] + (dl[q] >> 9);
-      s_v[p] = vr[q];
+      s_v[p] = VALS ? vr[q] : vals[wbase + q * 32 + lane];
       s_k[p] = kr[q];
     }
   }
