@@ -146,10 +146,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
   for (int q = 0; q < kScanItems; ++q) v += vals[q];
   uint32_t ex;
   const uint32_t T = block_exclusive_scan<kScanThreads>(v, ex, s_warp);
+  const unsigned long long hiA = (unsigned long long)((epoch << 2) | 1u) << 32;
+  const unsigned long long hiP = (unsigned long long)((epoch << 2) | 2u) << 32;
+  if (threadIdx.x == 0) st_relaxed_u64(look + bid, (bid == 0 ? hiP : hiA) | T);
+  __shared__ uint2 s_kv[HasStage<Out>::value ? kScanTile : 1];
+  if constexpr (HasStage<Out>::value) {  // stage before the look-back: overlaps its wait
+    uint32_t loc = ex;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q)
+      if (base + q < n && vals[q]) s_kv[loc++] = out.stage(base + q);
+  }
   if (threadIdx.x == 0) {
-    const unsigned long long hiA = (unsigned long long)((epoch << 2) | 1u) << 32;
-    const unsigned long long hiP = (unsigned long long)((epoch << 2) | 2u) << 32;
-    st_relaxed_u64(look + bid, (bid == 0 ? hiP : hiA) | T);
     uint32_t excl = 0;
     if (bid > 0) {
       excl = lookback4(look + (bid - 1), (long long)bid, 1, epoch);
@@ -161,12 +168,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_onepass(
   }
   __syncthreads();
   if constexpr (HasStage<Out>::value) {  // flags -> compacted pairs, coalesced writes
-    __shared__ uint2 s_kv[kScanTile];
-    uint32_t loc = ex;
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q)
-      if (base + q < n && vals[q]) s_kv[loc++] = out.stage(base + q);
-    __syncthreads();
     const uint32_t pre = s_pre;
     for (uint32_t p = threadIdx.x; p < T; p += kScanThreads) out.put(pre + p, s_kv[p]);
   } else if constexpr (HasStore8<Out>::value) {
