@@ -292,7 +292,10 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
 // by onesweep passes (one histogram kernel + one kernel per digit).  The
 // result lands in (kA, vA) after the swaps (the pointers are swapped here).
 // aggmask bit p: digit p is skewed (band mode), aggregate its histogram.
-constexpr int kOneItems = 16;
+// 18 items per thread at 4 CTAs/SM (measured: sort stage 3.39 -> 3.25 ms at
+// config C and 21.2 -> 20.3 ms at D against 16 items at 5 CTAs/SM; 12 items
+// at 6 CTAs/SM 3.70 ms; 20 items exceed the 48 KB static shared memory)
+constexpr int kOneItems = 18;
 cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uint32_t*& vB,
                      long long n, int shift0, int npass, unsigned aggmask = 0,
                      bool hist_ready = false, uint32_t slotK = 0) {
@@ -325,7 +328,7 @@ cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uin
       CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
       c->epoch = 1;
     }
-    k_radix_onesweep<kOneItems, 7, 5><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+    k_radix_onesweep<kOneItems, 7, 4><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
         kA, vA, kB, vB, n, shift0 + 8 * p, gh + 256 * p, P_<unsigned long long>(c->look),
         ctr + p, c->epoch, p == npass - 1 ? slotK : 0u);
     CR_LAUNCHED(c);

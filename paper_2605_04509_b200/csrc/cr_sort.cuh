@@ -449,10 +449,11 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
 // VAR bit 0: full tiles skip the bounds checks; bit 1: scatter into shared
 // memory before the look-back (the wait overlaps the local scatter); bit 2:
 // values loaded at the scatter, not held in registers through the ranking.
-// Shipped: VAR = 7 at 5 CTAs/SM (measured at config C, sort stage: 4.26 ms
-// for VAR = 0 at 3 CTAs/SM; 3.94 bit 0; 4.11 bit 1; 3.64 bits 0+1; 3.55 bits
-// 0+1 at 4 CTAs/SM; 3.40 VAR = 7 at 5 CTAs/SM; 12 items at 6 CTAs/SM and
-// keys re-read at the scatter were slower).
+// Shipped: VAR = 7, 18 items at 4 CTAs/SM (measured at config C, sort stage
+// with 16 items: 4.26 ms for VAR = 0 at 3 CTAs/SM; 3.94 bit 0; 4.11 bit 1;
+// 3.64 bits 0+1; 3.55 bits 0+1 at 4 CTAs/SM; 3.40 VAR = 7 at 5 CTAs/SM; 18
+// items at 4 CTAs/SM 3.25; 12 items at 6 CTAs/SM and keys re-read at the
+// scatter were slower).
 template <int ITEMS, bool FULL, bool VALS>
 __device__ __forceinline__ void onesweep_rank(const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals, long long n,
