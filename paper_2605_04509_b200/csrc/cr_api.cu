@@ -116,6 +116,7 @@ struct cr_ctx {
   float znear = 0.01f;
   // frame buffers
   DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, slots, biglist;
+  DevBuf bigcnt, bigmask, bigwlo, biginfo;  // union rows of big records (k_count_big)
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
   DevBuf hist, scalars, S, E, stage_out, frames;
@@ -437,7 +438,8 @@ void cr_destroy(cr_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
-                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
+                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->bigcnt,
+                   &c->bigmask, &c->bigwlo, &c->biginfo, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->hist, &c->look, &c->slook,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
@@ -779,6 +781,14 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->offs, Rz * 4));
   CR_TRY(ensure(c, c->slots, Rz * 64));
   CR_TRY(ensure(c, c->biglist, Rz * 4));
+  // stored union rows for up to 1/64 of the records (0.66 % are big at config C)
+  const size_t bcap = std::max<size_t>(4096, Rz / 64);
+  CR_TRY(ensure(c, c->bigcnt, bcap * kStoreRows * 4));
+  CR_TRY(ensure(c, c->bigmask, bcap * kStoreRows * 8));
+  CR_TRY(ensure(c, c->bigwlo, bcap * kStoreRows * 4));
+  CR_TRY(ensure(c, c->biginfo, bcap * 4));
+  const BigRows bigrows{P_<uint32_t>(c->bigcnt), P_<unsigned long long>(c->bigmask),
+                        P_<int>(c->bigwlo), P_<int>(c->biginfo), (uint32_t)bcap};
   int G = 1;
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
@@ -864,7 +874,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_LAUNCHED(c);                                                                             \
   k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                   \
       P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
-      P_<uint32_t>(c->cnt))
+      P_<uint32_t>(c->cnt), bigrows)
     switch (G) {
       case 1: CR_COUNTS(1); break;
       case 2: CR_COUNTS(2); break;
@@ -911,7 +921,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 #define CR_EMITB(GG)                                                                        \
   k_emit_big<GG><<<bin_grid, kBinThreads, cam_smem, c->side>>>(                              \
       rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->biglist), sc + 6, P_<float4>(c->mean4), \
-      P_<float4>(c->geom), tA, pA)
+      P_<float4>(c->geom), tA, pA, bigrows)
       switch (G) {
         case 1: CR_EMITB(1); break;
         case 2: CR_EMITB(2); break;

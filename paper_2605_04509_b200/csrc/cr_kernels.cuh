@@ -273,7 +273,8 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
                                 uint32_t* __restrict__ row_cnt, const uint32_t* __restrict__ row_off,
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
                                 uint32_t payload, unsigned long long* __restrict__ row_mask = nullptr,
-                                int* __restrict__ row_wlo = nullptr, int* __restrict__ wide = nullptr) {
+                                int* __restrict__ row_wlo = nullptr, int* __restrict__ wide = nullptr,
+                                int row_cap = 1 << 30, int* __restrict__ nrows_out = nullptr) {
   // MODE 0: count the group's rows; MODE 3: also store per-row counts in
   // row_cnt[it] (and, with row_mask, the row's 64-column window mask and the
   // tile id of its bit 0; *wide = 1 if a row needs more than one window);
@@ -296,6 +297,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
   const int rmin = max(gmin<G>(vis ? ty0 : 0x7fffffff), c_fp.row0);
   const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
   const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
+  if (MODE == 3 && nrows_out && (threadIdx.x & 31) == 0) *nrows_out = nrows;
   const int mine = nrows > it0 ? (nrows - it0 + istep - 1) / istep : 0;
   const int it_max = __reduce_max_sync(0xffffffffu, mine);
   const bool lead = (threadIdx.x & (G - 1)) == 0;
@@ -345,14 +347,14 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
           rowpos += (uint32_t)pc;
         }
         rown += (uint32_t)pc;
-        if (MODE == 3 && row_mask && lead && rowok && wi == 0) {
+        if (MODE == 3 && row_mask && lead && rowok && wi == 0 && it < row_cap) {
           row_mask[it] = mask;
           row_wlo[it] = (int)(rowbase + (uint32_t)wlo);  // tile id of the mask's bit 0
         }
       }
     }
     if (MODE == 3 && row_mask && lead && rowok && nwin > 1) *wide = 1;
-    if (MODE == 3 && lead && rowok) row_cnt[it] = rown;
+    if (MODE == 3 && lead && rowok && it < row_cap) row_cnt[it] = rown;
     n += rown;
   }
   return n;
@@ -896,19 +898,34 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
 // columns): one WARP per record; its 32/G groups each compute all views and
 // take interleaved union rows (it = g, g + 32/G, ...).
 // ===========================================================================
+// Union rows of the first cap big records, kept by k_count_big for k_emit_big
+// (record g: rows [g*kStoreRows, (g+1)*kStoreRows) relative to its first union
+// row; info[g] = number of union rows, or -1 when a row needs more than one
+// 64-column window or the union has more than kStoreRows rows: recompute).
+constexpr int kStoreRows = 64;
+struct BigRows {
+  uint32_t* cnt;
+  unsigned long long* mask;
+  int* wlo;
+  int* info;
+  uint32_t cap;
+};
+
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __restrict__ big,
                                                            const uint32_t* __restrict__ recs,
                                                            const uint32_t* __restrict__ n_ptr,
                                                            const float4* __restrict__ mean4,
                                                            const float4* __restrict__ geom,
-                                                           uint32_t* __restrict__ cnt) {
+                                                           uint32_t* __restrict__ cnt,
+                                                           BigRows st) {
   extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic: N * 68 B)
+  __shared__ int s_nr[kBinWarps];
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
   constexpr int GPW = 32 / G;
-  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G;
+  const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * kBinWarps;
   for (uint32_t g = (blockIdx.x * kBinThreads + threadIdx.x) / 32; g < n; g += nwarps) {
     const uint32_t o = big[g];
@@ -916,10 +933,26 @@ __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __res
     const int k = (int)fdiv(r, c_fp.divM);
     const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
     const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
-    const uint32_t c = group_union<0, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr,
-                                         nullptr, nullptr, nullptr, 0);
+    uint32_t c;
+    if (g < st.cap) {  // also keep the union's rows (counts, window masks) for k_emit_big
+      const size_t b = (size_t)g * kStoreRows;
+      if (lane == 0) st.info[g] = 0;  // the wide flag until the end
+      __syncwarp();
+      c = group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, st.cnt + b, nullptr,
+                            nullptr, nullptr, 0, st.mask + b, st.wlo + b, &st.info[g], kStoreRows,
+                            &s_nr[w]);
+      __syncwarp();
+      if (lane == 0) {
+        const int nr = s_nr[w];
+        st.info[g] = (st.info[g] != 0 || nr > kStoreRows) ? -1 : nr;  // -1: recompute
+      }
+    } else {
+      c = group_union<0, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, nullptr,
+                            nullptr, nullptr, 0);
+    }
     const uint32_t tot = __reduce_add_sync(0xffffffffu, v == 0 ? c : 0u);
     if (lane == 0) cnt[o] = tot;
+    __syncwarp();
   }
 }
 
@@ -929,7 +962,7 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
     const uint32_t* __restrict__ elist, const uint32_t* __restrict__ n_ptr,
     const float4* __restrict__ mean4, const float4* __restrict__ geom,
-    uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v) {
+    uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v, BigRows st) {
   extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic)
   __shared__ uint32_t s_rows[kBinWarps][kMaxRows];
   __shared__ unsigned long long s_rmask[kBinWarps][kMaxRows];  // per row: window mask
@@ -951,9 +984,23 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     for (int q = lane; q < kMaxRows; q += 32) rows[q] = 0;
     if (lane == 0) s_wide[w] = 0;
     __syncwarp();
-    // per-row counts and window masks (rows relative to the union's first row)
-    group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
-                      nullptr, 0, s_rmask[w], s_rwlo[w], &s_wide[w]);
+    // per-row counts and window masks (rows relative to the union's first row):
+    // stored by k_count_big, else recomputed
+    const int info = g < st.cap ? st.info[g] : -1;
+    if (info >= 0) {
+      const size_t b = (size_t)g * kStoreRows;
+      for (int q = lane; q < info; q += 32) {
+        const uint32_t cq = st.cnt[b + q];
+        rows[q] = cq;
+        if (cq) {
+          s_rmask[w][q] = st.mask[b + q];
+          s_rwlo[w][q] = st.wlo[b + q];
+        }
+      }
+    } else {
+      group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
+                        nullptr, 0, s_rmask[w], s_rwlo[w], &s_wide[w]);
+    }
     __syncwarp();
     // exclusive scan of the per-row counts -> row offsets (in place)
     uint32_t carry = offs[e];
