@@ -792,10 +792,6 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   int G = 1;
   while (G < s) G <<= 1;
   const unsigned bin_grid = (unsigned)(148 * 8);
-  // k_countv: 16 blocks per resident slot, so the grid-stride tail is short
-  // (measured at config C: binning 6.38 ms at 148 x 8 blocks, 6.27 at x16,
-  // 6.20 at x32, 6.14 at x64, 6.18 at x128)
-  const unsigned count_grid = (unsigned)(148 * 64);
   const size_t cam_smem = (size_t)N * kCamStride * sizeof(float);  // cameras staged per CTA
   uint32_t nvis = 0;
   uint32_t drange_h[2] = {0u, 0u};
@@ -861,6 +857,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   const int tpass = (tbits + 7) / 8;
   if (nvis > 0) {
     // count in (k, depth, i) order: position-indexed counts and union slots
+    // k_countv: 16 blocks per resident slot, so the grid-stride tail is short
+    // (measured at config C: binning 6.38 ms at 148 x 8 blocks, 6.27 at x16,
+    // 6.20 at x32, 6.14 at x64, 6.18 at x128); small frames: no more blocks
+    // than 64-record blocks of work
+    const unsigned count_grid =
+        (unsigned)std::min<long long>(148 * 64, std::max<long long>(148, ((long long)nvis + 63) / 64));
 #define CR_COUNTS(GG)                                                                         \
   if (GG == 32 && s <= 24) /* 17..24 views: three per lane, 8-lane groups (P4K s=18:      \
                                 binning 9.2 -> 8.3 ms vs 16 lanes x 2 views) */              \
