@@ -21,6 +21,11 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# Mutation testing only (tools/oracle_mutations.py): build a planted-mutation
+# copy of oracle.cpp instead, into its own library next to it.
+if os.environ.get("CR_ORACLE_MUTANT_SRC"):
+    _SRC = os.environ["CR_ORACLE_MUTANT_SRC"]
+    _LIB = os.path.splitext(_SRC)[0] + ".so"
 _FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC", "-shared",
           "-pthread"]
 _lock = threading.Lock()
@@ -73,6 +78,7 @@ def _bind(L):
     sig("cro_create", vp, C.c_int)
     sig("cro_destroy", None, vp)
     sig("cro_threads", C.c_int, vp)
+    sig("cro_set_tile_pad", None, vp, C.c_float)
     sig("cro_set_scene", C.c_int, vp, C.c_int64, C.c_int, _f32p, _f32p, _f32p, _f32p, _f32p)
     sig("cro_get_constants", None, vp, _f32p, _f32p)
     sig("cro_set_display_tan", C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
@@ -201,6 +207,10 @@ class Oracle:
     @property
     def threads(self) -> int:
         return self._L.cro_threads(self._c)
+
+    def set_tile_pad(self, pad: float):
+        """Test knob: grow every tile rectangle of the tile test by pad px."""
+        self._L.cro_set_tile_pad(self._c, float(pad))
 
     def set_scene(self, scene):
         M = int(scene["means"].shape[0])

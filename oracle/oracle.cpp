@@ -192,21 +192,24 @@ bool cov2d(const Cam& c, const CamConst& k, const P3& p, const float* S6, float*
 // O7 — AccuTile reading: tiles whose pixel-centre rectangle
 // meets the ellipse {m + d : d^T Sigma^-1 d <= tau}.  Row range of one view.
 struct RowRange { int ty0, ty1; float ex, ey; };
-RowRange row_range(float mx, float my, float a, float c, float tau, int TY) {
+// `pad` (test knob, default 0) grows every tile rectangle by pad pixels on each
+// side: the superfluous-keys check of S:392 / P:379-382.  With pad = 0 every
+// expression below is bit-identical to the unpadded reading (x - 0 = x).
+RowRange row_range(float mx, float my, float a, float c, float tau, int TY, float pad = 0.0f) {
     RowRange r;
     r.ex = std::sqrt(tau * a);
     r.ey = std::sqrt(tau * c);
-    r.ty0 = clamp_to_int(std::ceil(((my - r.ey) - 15.5f) / 16.0f), 0.0f, (float)TY);
-    r.ty1 = clamp_to_int(std::floor(((my + r.ey) - 0.5f) / 16.0f), -1.0f, (float)(TY - 1));
+    r.ty0 = clamp_to_int(std::ceil((((my - r.ey) - 15.5f) - pad) / 16.0f), 0.0f, (float)TY);
+    r.ty1 = clamp_to_int(std::floor((((my + r.ey) - 0.5f) + pad) / 16.0f), -1.0f, (float)(TY - 1));
     return r;
 }
 // Tile columns [tx0, tx1] hit in row ty (empty if tx0 > tx1).  Returns false
 // if the row band misses the ellipse.
 bool row_cols(float mx, float my, float a, float b, float c, float det, float tau,
-              const RowRange& rr, int ty, int TX, int* tx0, int* tx1) {
+              const RowRange& rr, int ty, int TX, int* tx0, int* tx1, float pad = 0.0f) {
     float ex = rr.ex, ey = rr.ey;
-    float dlo = mxf((16.0f * (float)ty + 0.5f) - my, -ey);
-    float dhi = mnf((16.0f * (float)ty + 15.5f) - my, ey);
+    float dlo = mxf(((16.0f * (float)ty + 0.5f) - pad) - my, -ey);
+    float dhi = mnf(((16.0f * (float)ty + 15.5f) + pad) - my, ey);
     if (dlo > dhi) return false;
     float dyR = (b * ex) / a;
     float dyL = -dyR;
@@ -217,8 +220,8 @@ bool row_cols(float mx, float my, float a, float b, float c, float det, float ta
     auto xl = [&](float dy) { return ((b * dy) - h(dy)) * ic; };
     float right = mx + ((dlo <= dyR && dyR <= dhi) ? ex : mxf(xr(dlo), xr(dhi)));
     float left = mx + ((dlo <= dyL && dyL <= dhi) ? -ex : mnf(xl(dlo), xl(dhi)));
-    *tx0 = clamp_to_int(std::ceil((left - 15.5f) / 16.0f), 0.0f, (float)TX);
-    *tx1 = clamp_to_int(std::floor((right - 0.5f) / 16.0f), -1.0f, (float)(TX - 1));
+    *tx0 = clamp_to_int(std::ceil(((left - 15.5f) - pad) / 16.0f), 0.0f, (float)TX);
+    *tx1 = clamp_to_int(std::floor(((right - 0.5f) + pad) / 16.0f), -1.0f, (float)(TX - 1));
     return true;
 }
 
@@ -321,6 +324,7 @@ struct cro_ctx {
     std::vector<float> img;      // band image [rows*16 clipped][W][3]
     int64_t n_evals = 0;
     int nthreads = 0;
+    float tile_pad = 0.0f;  // test knob: grow tile rectangles by this many pixels
 };
 
 extern "C" {
@@ -398,6 +402,9 @@ cro_ctx* cro_create(int nthreads) {
 }
 void cro_destroy(cro_ctx* c) { delete c; }
 int cro_threads(const cro_ctx* c) { return c->nthreads; }
+// Superfluous-keys check: grow every tile's pixel-centre
+// rectangle by pad pixels in the tile test (O7).  0 = the reading itself.
+void cro_set_tile_pad(cro_ctx* c, float pad) { c->tile_pad = pad; }
 
 // D1: Gaussians, SoA fp32, quats (w,x,y,z), linear scales, post-sigmoid
 // opacity, sh[M][(deg+1)^2][3].  O4 constants computed here.
@@ -586,7 +593,7 @@ int cro_render(cro_ctx* c, int s, int row0, int row1, const float* bg,
                     vok[l] = pj.z >= c->znear;
                     if (!vok[l]) continue;
                     mean2d(c->cams[j], pj, &vmx[l], &vmy[l]);
-                    vrr[l] = row_range(vmx[l], vmy[l], a, cc, c->tau[i], TY);
+                    vrr[l] = row_range(vmx[l], vmy[l], a, cc, c->tau[i], TY, c->tile_pad);
                     rmin = std::min(rmin, vrr[l].ty0);
                     rmax = std::max(rmax, vrr[l].ty1);
                 }
@@ -600,7 +607,7 @@ int cro_render(cro_ctx* c, int s, int row0, int row1, const float* bg,
                         if (!vok[l] || ty < vrr[l].ty0 || ty > vrr[l].ty1) continue;
                         int tx0, tx1;
                         if (!row_cols(vmx[l], vmy[l], a, b, cc, det, c->tau[i], vrr[l], ty, TX,
-                                      &tx0, &tx1))
+                                      &tx0, &tx1, c->tile_pad))
                             continue;
                         if (tx0 <= tx1) iv.push_back({tx0, tx1});
                     }
