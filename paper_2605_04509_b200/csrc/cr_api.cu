@@ -138,7 +138,6 @@ struct cr_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
-  int exp = 0;         // CR_EXP: kernel-variant A/B experiments (read per render)
   bool motion_bound = false;  // pre-cull by the cluster motion bound (narrow clusters)
 };
 
@@ -490,7 +489,9 @@ cr_status cr_upload_gaussians(cr_ctx* c, int64_t M, int deg, const float* means,
   }
   for (long long i = 0; i < M; ++i) {
     if (!std::isfinite(h_op[i])) return fail(c, CR_ERR_NONFINITE, "opacity %lld not finite", i);
-    h_tau[i] = (float)(2.0 * std::log(255.0 * (double)h_op[i]));
+    if (!(h_op[i] >= 0.0f && h_op[i] <= 1.0f))
+      return fail(c, CR_ERR_INVALID_ARG, "opacity %lld = %g outside [0,1]", i, (double)h_op[i]);
+    h_tau[i] = (float)(2.0 * std::log(255.0 * (double)h_op[i]));  // o = 0: -inf, culled (O4)
   }
   const size_t nin = (size_t)M * (3 + 4 + 3 + 1 + 1 + nc3);
   CR_TRY(ensure(c, c->tmp, nin * 4));
@@ -504,22 +505,24 @@ cr_status cr_upload_gaussians(cr_ctx* c, int64_t M, int deg, const float* means,
   CR_CUDA(c, cudaMemcpyAsync(d_op, h_op.data(), 4 * M, cudaMemcpyHostToDevice, c->stream));
   CR_CUDA(c, cudaMemcpyAsync(d_tau, h_tau.data(), 4 * M, cudaMemcpyHostToDevice, c->stream));
   CR_CUDA(c, cudaMemcpyAsync(d_sh, sh, 4 * (size_t)M * nc3, kind, c->stream));
-  CR_TRY(ensure(c, c->mean4, 16 * (size_t)M));
-  CR_TRY(ensure(c, c->cov8, 32 * (size_t)M));
-  CR_TRY(ensure(c, c->shsoa, 4 * (size_t)M * nc3));
+  // validate the staged copy first: a rejected upload keeps the previous scene
   int* flag = P_<int>(c->scalars) + 7;
   CR_CUDA(c, cudaMemsetAsync(flag, 0, 4, c->stream));
-  k_upload<<<grid_for(M, 256), 256, 0, c->stream>>>(M, nc3, d_means, d_quats, d_scales, d_op,
-                                                     d_tau, d_sh, P_<float4>(c->mean4),
-                                                     P_<float4>(c->cov8), P_<float>(c->shsoa),
-                                                     flag);
+  k_validate<<<148 * 8, 256, 0, c->stream>>>((long long)(d_op - d_means), d_means, flag);
+  CR_LAUNCHED(c);
+  k_validate<<<148 * 8, 256, 0, c->stream>>>((long long)M * nc3, d_sh, flag);
   CR_LAUNCHED(c);
   uint32_t bad = 0;
   CR_TRY(read_u32(c, (const uint32_t*)flag, &bad));
-  if (bad) {
-    c->has_scene = false;
-    return fail(c, CR_ERR_NONFINITE, "NaN/Inf in uploaded Gaussians");
-  }
+  if (bad) return fail(c, CR_ERR_NONFINITE, "NaN/Inf in uploaded Gaussians");
+  c->has_scene = false;  // the scene buffers may be reallocated from here on
+  CR_TRY(ensure(c, c->mean4, 16 * (size_t)M));
+  CR_TRY(ensure(c, c->cov8, 32 * (size_t)M));
+  CR_TRY(ensure(c, c->shsoa, 4 * (size_t)M * nc3));
+  k_upload<<<grid_for(M, 256), 256, 0, c->stream>>>(M, nc3, d_means, d_quats, d_scales, d_op,
+                                                     d_tau, d_sh, P_<float4>(c->mean4),
+                                                     P_<float4>(c->cov8), P_<float>(c->shsoa));
+  CR_LAUNCHED(c);
   c->M = M;
   c->deg = deg;
   c->has_scene = true;
@@ -651,10 +654,6 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (R > 0xFFFFFFFFLL) return fail(c, CR_ERR_CAPACITY, "K*M = %lld exceeds 2^32", R);
   cudaSetDevice(c->device);
   c->launches = 0;
-  {
-    const char* ex = getenv("CR_EXP");
-    c->exp = ex ? atoi(ex) : 0;
-  }
   c->has_frame = false;
   cudaStream_t str = c->stream;
 

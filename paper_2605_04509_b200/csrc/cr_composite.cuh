@@ -28,7 +28,7 @@ namespace cr {
 #define CR_COMP_MINB 10  // measured: 48 regs, 11.04 vs 11.17 ms at config C
 #endif
 constexpr int kCompWarps = 4;
-constexpr int kMaxChunks = 128;
+constexpr int kMaxChunks = kMaxViews + 24;  // k_chunks_build emits <= K + 24 per tile
 constexpr int kSlots = 8;  // distinct views staged per pass of a chunk
 
 __device__ __forceinline__ float ex2_approx(float x) {

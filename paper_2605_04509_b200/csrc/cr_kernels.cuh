@@ -132,26 +132,33 @@ __global__ void k_chunks_build(const uint8_t* __restrict__ V, const uint16_t* __
 // order as written in DESIGN.md O4), SH transposed to coefficient-major SoA.
 // mean4 = (mu, tau), cov8 = {S00,S01,S02,S11},{S12,S22,o,0}.
 // ===========================================================================
+// Validation pass over the staged inputs: any NaN/Inf sets *nonfinite.
+// Runs before the scene buffers are touched, so a rejected upload leaves the
+// previous scene intact (header: "on error the context keeps its state").
+__global__ void k_validate(long long n, const float* __restrict__ x, int* __restrict__ nonfinite) {
+  bool bad = false;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[q]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
 __global__ void k_upload(long long M, int nc3, const float* __restrict__ means,
                          const float* __restrict__ quats, const float* __restrict__ scales,
                          const float* __restrict__ opac, const float* __restrict__ tau,
                          const float* __restrict__ sh, float4* __restrict__ mean4,
-                         float4* __restrict__ cov8, float* __restrict__ shsoa,
-                         int* __restrict__ nonfinite) {
+                         float4* __restrict__ cov8, float* __restrict__ shsoa) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= M) return;
-  bool bad = false;
   float q4[4], s3[3], m3[3];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) { q4[a] = quats[4 * i + a]; bad |= !isfinite(q4[a]); }
+  for (int a = 0; a < 4; ++a) q4[a] = quats[4 * i + a];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     s3[a] = scales[3 * i + a];
     m3[a] = means[3 * i + a];
-    bad |= !isfinite(s3[a]) || !isfinite(m3[a]);
   }
   const float o = opac[i];
-  bad |= !isfinite(o);
   double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
   const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)),
                                                   __dmul_rn(y, y)),
@@ -183,12 +190,7 @@ __global__ void k_upload(long long M, int nc3, const float* __restrict__ means,
   mean4[i] = make_float4(m3[0], m3[1], m3[2], tau[i]);
   cov8[2 * i] = make_float4(c6[0], c6[1], c6[2], c6[3]);
   cov8[2 * i + 1] = make_float4(c6[4], c6[5], o, 0.0f);
-  for (int q = 0; q < nc3; ++q) {
-    const float v = sh[(long long)i * nc3 + q];
-    bad |= !isfinite(v);
-    shsoa[(long long)q * M + i] = v;
-  }
-  if (bad) atomicOr(nonfinite, 1);
+  for (int q = 0; q < nc3; ++q) shsoa[(long long)q * M + i] = sh[(long long)i * nc3 + q];
 }
 
 // ===========================================================================
@@ -274,12 +276,15 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
                                 uint32_t* __restrict__ out_t, uint32_t* __restrict__ out_v,
                                 uint32_t payload, unsigned long long* __restrict__ row_mask = nullptr,
                                 int* __restrict__ row_wlo = nullptr, int* __restrict__ wide = nullptr,
-                                int row_cap = 1 << 30, int* __restrict__ nrows_out = nullptr) {
+                                int row_cap = 1 << 30, int* __restrict__ nrows_out = nullptr,
+                                int wbeg = 0, int wend = 1 << 30) {
   // MODE 0: count the group's rows; MODE 3: also store per-row counts in
-  // row_cnt[it] (and, with row_mask, the row's 64-column window mask and the
-  // tile id of its bit 0; *wide = 1 if a row needs more than one window);
-  // MODE 2: write the tiles of row it at row_off[it] + rank.
-  // The group handles union rows it = it0, it0 + istep, ...
+  // row_cnt[it - wbeg] (and, with row_mask, the row's 64-column window mask and
+  // the tile id of its bit 0; *wide = 1 if a row needs more than one window);
+  // MODE 2: write the tiles of row it at row_off[it - wbeg] + rank.
+  // The group handles union rows it = it0, it0 + istep, ... restricted to the
+  // row window [wbeg, wend) (callers with bounded per-row arrays walk a tall
+  // union window by window); stores need it - wbeg < row_cap.
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int j = k * s + v;
   bool vis = false;
@@ -298,14 +303,18 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
   const int rmax = min(gmax<G>(vis ? ty1 : -1), c_fp.row1 - 1);
   const int nrows = (active && rmax >= rmin) ? rmax - rmin + 1 : 0;
   if (MODE == 3 && nrows_out && (threadIdx.x & 31) == 0) *nrows_out = nrows;
-  const int mine = nrows > it0 ? (nrows - it0 + istep - 1) / istep : 0;
+  const int rend = min(nrows, wend);
+  const int mine = rend > it0 ? (rend - it0 + istep - 1) / istep : 0;
+  const int ii_lo = wbeg > it0 ? (wbeg - it0 + istep - 1) / istep : 0;
   const int it_max = __reduce_max_sync(0xffffffffu, mine);
+  const int ii_min = __reduce_min_sync(0xffffffffu, (unsigned)ii_lo);
   const bool lead = (threadIdx.x & (G - 1)) == 0;
   uint32_t n = 0;
-  for (int ii = 0; ii < it_max; ++ii) {
+  for (int ii = ii_min; ii < it_max; ++ii) {
     const int it = it0 + ii * istep;
     const int ty = rmin + it;
-    const bool rowok = ii < mine;
+    const int il = it - wbeg;  // index into the window's per-row arrays
+    const bool rowok = ii < mine && ii >= ii_lo;
     int tx0 = 0x7fffffff, tx1 = -1;
     if (rowok && vis && ty >= ty0 && ty <= ty1) {
       int q0, q1;
@@ -317,7 +326,7 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
     const int lo = gmin<G>(tx0), hi = gmax<G>(tx1);
     const bool any = rowok && hi >= lo;
     const uint32_t rowbase = (uint32_t)ty * (uint32_t)TX;
-    uint32_t rowpos = (MODE == 2 && rowok) ? row_off[it] : 0u;
+    uint32_t rowpos = (MODE == 2 && rowok) ? row_off[il] : 0u;
     uint32_t rown = 0;
     // merge the views' intervals in 64-column windows (one window unless the
     // row spans >= 64 tiles), warp-uniform window count
@@ -347,14 +356,14 @@ __device__ uint32_t group_union(const float* s_cam, bool active, int k, int v, f
           rowpos += (uint32_t)pc;
         }
         rown += (uint32_t)pc;
-        if (MODE == 3 && row_mask && lead && rowok && wi == 0 && it < row_cap) {
-          row_mask[it] = mask;
-          row_wlo[it] = (int)(rowbase + (uint32_t)wlo);  // tile id of the mask's bit 0
+        if (MODE == 3 && row_mask && lead && rowok && wi == 0 && il < row_cap) {
+          row_mask[il] = mask;
+          row_wlo[il] = (int)(rowbase + (uint32_t)wlo);  // tile id of the mask's bit 0
         }
       }
     }
     if (MODE == 3 && row_mask && lead && rowok && nwin > 1) *wide = 1;
-    if (MODE == 3 && lead && rowok && it < row_cap) row_cnt[it] = rown;
+    if (MODE == 3 && lead && rowok && il < row_cap) row_cnt[il] = rown;
     n += rown;
   }
   return n;
@@ -956,7 +965,9 @@ __global__ void __launch_bounds__(kBinThreads) k_count_big(const uint32_t* __res
   }
 }
 
-constexpr int kMaxRows = 288;  // >= TY for 8K (270 tile rows)
+// Per-warp row arrays hold kMaxRows union rows; a taller union (panels over
+// 16 * kMaxRows px, tall bands) is written window by window.
+constexpr int kMaxRows = 288;
 template <int G>
 __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const uint32_t* __restrict__ rec_sorted, const uint32_t* __restrict__ offs,
@@ -968,6 +979,7 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
   __shared__ unsigned long long s_rmask[kBinWarps][kMaxRows];  // per row: window mask
   __shared__ int s_rwlo[kBinWarps][kMaxRows];                  // per row: window column
   __shared__ int s_wide[kBinWarps];
+  __shared__ int s_nr[kBinWarps];
   stage_cams(s_cam);
   __syncthreads();
   const uint32_t n = *n_ptr;
@@ -981,63 +993,70 @@ __global__ void __launch_bounds__(kBinThreads) k_emit_big(
     const int k = (int)fdiv(r, c_fp.divM);
     const float4 m = mean4[(long long)r - (long long)k * c_fp.M];
     const EllRec el = ell_load(geom[2ull * r], geom[2ull * r + 1]);
-    for (int q = lane; q < kMaxRows; q += 32) rows[q] = 0;
-    if (lane == 0) s_wide[w] = 0;
-    __syncwarp();
     // per-row counts and window masks (rows relative to the union's first row):
-    // stored by k_count_big, else recomputed
+    // stored by k_count_big (<= kStoreRows rows), else recomputed per window
     const int info = g < st.cap ? st.info[g] : -1;
-    if (info >= 0) {
-      const size_t b = (size_t)g * kStoreRows;
-      for (int q = lane; q < info; q += 32) {
-        const uint32_t cq = st.cnt[b + q];
-        rows[q] = cq;
-        if (cq) {
-          s_rmask[w][q] = st.mask[b + q];
-          s_rwlo[w][q] = st.wlo[b + q];
-        }
-      }
-    } else {
-      group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
-                        nullptr, 0, s_rmask[w], s_rwlo[w], &s_wide[w]);
-    }
-    __syncwarp();
-    // exclusive scan of the per-row counts -> row offsets (in place)
     uint32_t carry = offs[e];
-    int nrows = 0;
-    for (int b0 = 0; b0 < kMaxRows; b0 += 32) {
-      const uint32_t x = rows[b0 + lane];
-      uint32_t incl = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    for (int wb = 0;; wb += kMaxRows) {
+      for (int q = lane; q < kMaxRows; q += 32) rows[q] = 0;
+      if (lane == 0) { s_wide[w] = 0; s_nr[w] = 0; }
+      __syncwarp();
+      if (info >= 0) {
+        const size_t b = (size_t)g * kStoreRows;
+        for (int q = lane; q < info; q += 32) {
+          const uint32_t cq = st.cnt[b + q];
+          rows[q] = cq;
+          if (cq) {
+            s_rmask[w][q] = st.mask[b + q];
+            s_rwlo[w][q] = st.wlo[b + q];
+          }
+        }
+        if (lane == 0) s_nr[w] = info;
+      } else {
+        group_union<3, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, rows, nullptr, nullptr,
+                          nullptr, 0, s_rmask[w], s_rwlo[w], &s_wide[w], kMaxRows, &s_nr[w], wb,
+                          wb + kMaxRows);
       }
-      rows[b0 + lane] = carry + incl - x;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-      nrows = max(nrows, __reduce_max_sync(0xffffffffu, x ? b0 + lane + 1 : 0));
-    }
-    __syncwarp();
-    if (s_wide[w]) {  // a row wider than one 64-column window: recompute and write
-      group_union<2, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, rows, out_t,
-                        out_v, r);
-    } else {  // every row from its stored window mask (no second union): lane per row
-      for (int it = lane; it < nrows; it += 32) {
-        uint32_t pos = rows[it];
-        const uint32_t end = it + 1 < nrows ? rows[it + 1] : carry;
-        if (end == pos) continue;  // empty row (its mask slot was not written)
-        unsigned long long mk = s_rmask[w][it];
-        const uint32_t tb = (uint32_t)s_rwlo[w][it];
-        while (mk) {
-          const int bit = __ffsll((long long)mk) - 1;
-          mk &= mk - 1;
-          out_t[pos] = tb + (uint32_t)bit;
-          out_v[pos] = r;
-          ++pos;
+      __syncwarp();
+      const int nr_all = s_nr[w];
+      // exclusive scan of the window's per-row counts -> row offsets (in place)
+      int nrows = 0;
+      for (int b0 = 0; b0 < kMaxRows; b0 += 32) {
+        const uint32_t x = rows[b0 + lane];
+        uint32_t incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        rows[b0 + lane] = carry + incl - x;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+        nrows = max(nrows, __reduce_max_sync(0xffffffffu, x ? b0 + lane + 1 : 0));
+      }
+      __syncwarp();
+      if (s_wide[w]) {  // a row wider than one 64-column window: recompute and write
+        group_union<2, G>(s_cam, true, k, v, m.x, m.y, m.z, el, gi, GPW, nullptr, rows, out_t,
+                          out_v, r, nullptr, nullptr, nullptr, kMaxRows, nullptr, wb,
+                          wb + kMaxRows);
+      } else {  // every row from its stored window mask (no second union): lane per row
+        for (int it = lane; it < nrows; it += 32) {
+          uint32_t pos = rows[it];
+          const uint32_t end = it + 1 < nrows ? rows[it + 1] : carry;
+          if (end == pos) continue;  // empty row (its mask slot was not written)
+          unsigned long long mk = s_rmask[w][it];
+          const uint32_t tb = (uint32_t)s_rwlo[w][it];
+          while (mk) {
+            const int bit = __ffsll((long long)mk) - 1;
+            mk &= mk - 1;
+            out_t[pos] = tb + (uint32_t)bit;
+            out_v[pos] = r;
+            ++pos;
+          }
         }
       }
+      __syncwarp();
+      if (info >= 0 || wb + kMaxRows >= nr_all) break;
     }
-    __syncwarp();
   }
 }
 

@@ -85,7 +85,6 @@ def save_ply(scene: dict, path=None) -> bytes:
     cols.append(("opacity", np.log(o / (1 - o))))
     cols += [(f"scale_{c}", np.log(scene["scales"][:, c])) for c in range(3)]
     cols += [(f"rot_{c}", scene["quats"][:, c]) for c in range(4)]
-    cols.sort(key=lambda kv: ["x", "y", "z"].index(kv[0]) if kv[0] in "xyz" else 0)
     dt = np.dtype([(nme, "<f4") for nme, _ in cols])
     arr = np.zeros(M, dt)
     for nme, val in cols:

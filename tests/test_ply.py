@@ -29,3 +29,14 @@ def test_activations_and_errors():
         ply.load_ply(blob[:-8])
     with pytest.raises(ply.PlyError, match="UnsupportedFormat"):
         ply.load_ply(blob.replace(b"binary_little_endian", b"ascii"))
+
+
+def test_header_property_order_is_inria():
+    # INRIA 3DGS vertex layout: x y z, f_dc_0..2, f_rest_*, opacity,
+    # scale_0..2, rot_0..3 — tools that read by position expect exactly this order.
+    blob = ply.save_ply(sy.random_scene(3, 1, 0))
+    head = blob[:blob.index(b"end_header")].decode().splitlines()
+    props = [ln.split()[-1] for ln in head if ln.startswith("property")]
+    rest = [f"f_rest_{i}" for i in range(9)]
+    assert props == (["x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2"] + rest + ["opacity"]
+                     + [f"scale_{i}" for i in range(3)] + [f"rot_{i}" for i in range(4)])
