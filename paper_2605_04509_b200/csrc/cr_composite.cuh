@@ -40,6 +40,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // Tolerance-path per-view mean (fast FMA / approximate reciprocal); far away
 // when the view cannot see the Gaussian (Z12) so that alpha underflows to 0.
 // The camera comes as 4 float4 {R0..R3}, {R4..R7}, {R8,t0,t1,t2}, {fx,fy,cx,cy}.
+// position of the most significant set bit (x != 0): one FLO
+__device__ __forceinline__ int msb_pos(unsigned x) {
+  int p;
+  asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(x));
+  return p;
+}
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -60,20 +66,28 @@ __device__ __forceinline__ float2 mean2d_fast(const CamDev& c, float mx, float m
 }
 
 // One blend step (Eq.10 alpha, Eq.9 accumulation; 0.99 clamp, 1/255 skip,
-// stop before blending when T(1-alpha) < 1e-4 — Z9).
+// stop before blending when T(1-alpha) < 1e-4 — Z9), tolerance-path math
+// shared by every composite kernel (so they agree bit for bit):
+//   g = (A', B', C', log2 o) with the conic prescaled by -log2(e)/2, -log2(e),
+//   -log2(e)/2, so q = power * log2(e) = A' dx^2 + B' dx dy + C' dy^2 (5 ops);
+//   the 1/255 skip is decided in the log domain before the exponential
+//   (t = q + log2 o >= log2(1/255)), so skipped entries never reach the MUFU;
+//   w = alpha T, T' = T - w, C += c w.
+constexpr float kLog2MinAlpha = -7.99435343685886f;  // log2(1/255)
 __device__ __forceinline__ void blend_step(const float4 g, const float2 m, const float col,
                                            const float px, const float py, float& T, float& C,
                                            bool& done) {
   const float dx = m.x - px, dy = m.y - py;
-  const float q = fmaf(g.x * dx, dx, fmaf(g.z * dy, dy, g.y * dx * dy));  // power*log2(e)
-  const float a = fminf(0.99f, ex2_approx(q + g.w));
-  const float alpha = (q <= 0.0f) ? a : 0.0f;  // power > 0: skip (folded, one branch)
-  if (alpha >= (1.0f / 255.0f)) {
-    const float Tn = T * (1.0f - alpha);
+  const float q = fmaf(dx, fmaf(g.x, dx, g.y * dy), (g.z * dy) * dy);
+  const float t = q + g.w;
+  if (t >= kLog2MinAlpha && q <= 0.0f) {  // power > 0 or alpha < 1/255: skip
+    const float alpha = fminf(0.99f, ex2_approx(t));
+    const float wgt = alpha * T;
+    const float Tn = T - wgt;
     if (Tn < 1e-4f) {
       done = true;
     } else {
-      C = fmaf(col, alpha * T, C);
+      C = fmaf(col, wgt, C);
       T = Tn;
     }
   }
@@ -234,10 +248,13 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
       for (uint32_t b = e0; b < e1; b += 32) {
         const Staged nxt = gather_entry(rec0, rec1, mean4, r_nxt, b + 32 + lane < e1, kM);
         r_nxt = (b + 64 + lane < e1) ? vals[b + 64 + lane] : 0u;
+        // entry of lane l is staged at slot 31 - l and the masks are bit-reversed,
+        // so the front-most remaining entry is the highest set bit (one FLO)
+        const int slot = 31 - lane;
         float hx = -1.f, hy = -1.f;
         if (cur.valid) {
-          s_rec[w][lane] = cur.r0;
-          s_col[w][lane] = cur.r1;
+          s_rec[w][slot] = cur.r0;
+          s_col[w][slot] = cur.r1;
           const __half2 ext = *reinterpret_cast<const __half2*>(&cur.r1.w);
           hx = __low2float(ext);
           hy = __high2float(ext);
@@ -246,7 +263,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
         for (int v = 0; v < ns; ++v) {
           const float2 mu = mean2d_fast4(s_cam4[w][v][0], s_cam4[w][v][1], s_cam4[w][v][2],
                                          s_cam4[w][v][3], cur.m.x, cur.m.y, cur.m.z);
-          s_mu[w][v][lane] = mu;
+          s_mu[w][v][slot] = mu;
           const float4 bx = s_box[w][v];
           const bool pass = cur.valid && fabsf(mu.x - bx.x) <= bx.z + hx &&
                             fabsf(mu.y - bx.y) <= bx.w + hy;
@@ -256,16 +273,25 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
         __syncwarp();
         const int n = min(32u, e1 - b);
         if (!done) {
-          unsigned mm = mymask;
+          unsigned mm = __brev(mymask);
           int qstop = -1;
+          const float2* mu_v = s_mu[w][sl];
+          // colour of channel u: 32-bit shared address kept in a register and
+          // loaded on every visit (cheaper than the address the compiler would
+          // otherwise rebuild inside the contributing branch)
+          const uint32_t col_a = (uint32_t)__cvta_generic_to_shared(&s_col[w][0].x + u);
           while (mm) {
-            const int q = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const float4 g = s_rec[w][q];
-            const float2 mu = s_mu[w][sl][q];
-            const float col = (&s_col[w][q].x)[u];
-            blend_step(g, mu, col, px, py, T, C, done);
-            if (done) { qstop = q; break; }
+            const int q = msb_pos(mm);
+            mm ^= 1u << q;
+            float col;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(col) : "r"(col_a + 16u * (uint32_t)q));
+            bool stop = false;
+            blend_step(s_rec[w][q], mu_v[q], col, px, py, T, C, stop);
+            if (stop) {
+              done = true;
+              qstop = 31 - q;
+              mm = 0u;
+            }
           }
           if (COUNT) nev += (qstop >= 0) ? (unsigned)(qstop + 1) : (unsigned)n;
         }
