@@ -36,10 +36,12 @@ METRICS = {"C": METRIC, "A": "interlaced LF frames/s (256x144, 8 views)",
            "P2K": "interlaced LF frames/s (1440x2560 portrait, 63 views, s=16)",
            "P4K": "interlaced LF frames/s (4K, 71 views, s=18)"}
 UNIT = "frames/s"
-# algorithmic FP32 operations per (subpixel, splat) evaluation of Eqs.9-10
-# (DESIGN.md §5): delta 2, quadratic form 8, x(-1/2) 1, exp 1, o*exp 1,
-# min 1, 1-alpha 1, T(1-alpha) 1, c*alpha*T 2, accumulate 1, tests 1.
-FLOPS_PER_EVAL = 20
+# algorithmic FP32 operations per (subpixel, splat) evaluation of Eqs.9-10,
+# SURVEY §8d's count: delta 2, quadratic form 5, alpha
+# (o exp, min) 3, transmittance 2, colour accumulation 2, tests 2 = 16,
+# plus one MUFU exponential per evaluation.
+FLOPS_PER_EVAL = 16
+MUFU_PER_EVAL = 1
 
 
 def load_peaks():
@@ -133,23 +135,6 @@ def oracle_sample(cfg, scene, cams, rows, nthreads=0):
                        "fraction / seconds (conservative: the per-frame preprocess is not "
                        "amortised over the band)"),
             "seconds": dt}
-
-
-def committed_ncu(kernel: str):
-    """(DRAM bytes per launch, issued IPC per SM) of `kernel` from the newest
-    committed ncu table (profiles/r*/ncu_kernels_configC.txt, tools/prof_all.sh)."""
-    import glob
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_kernels_configC.txt")),
-                    reverse=True):
-        for ln in open(f):
-            p = ln.split()
-            if p and p[0].startswith(kernel) and len(p) >= 7:
-                try:  # columns: name.. n time_ms dram_GB GB/s IPC occ%
-                    return (float(p[-4]) * 1e9 / int(p[-6]), float(p[-2]),
-                            os.path.relpath(f, ROOT))
-                except ValueError:
-                    pass
-    return None, None, None
 
 
 def cpu_model():
@@ -328,34 +313,47 @@ def main():
     info = dict(r.last_stats)
     torch.cuda.synchronize()
 
-    # ---- timed region (stats on: per-stage CUDA events on the render stream)
+    # ---- per-stage breakdown (untimed: stats synchronise after every frame)
     ms_stage = {"preprocess": 0.0, "bin": 0.0, "sort": 0.0, "composite": 0.0, "total": 0.0}
-    launches = 0
+    nstage = min(5, args.steps)
+    launches_per_step = 0
+    for _ in range(nstage):
+        step(stats=True)
+        st = r.last_stats
+        for k in ms_stage:
+            ms_stage[k] += st["ms_" + k] / nstage
+        launches_per_step = st["launches"]
+    peak_ctx_bytes = int(r.last_stats["device_bytes"])
+
+    # ---- timed region: back-to-back frames, a CUDA event after every step
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step(stats=True)
-            st = r.last_stats
-            for k in ms_stage:
-                ms_stage[k] += st["ms_" + k]
-            launches += st["launches"]
-        e1.record(stream)
+        evs[0].record(stream)
+        for q in range(args.steps):
+            step()
+            evs[q + 1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    elapsed = e0.elapsed_time(e1)  # ms
-    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    step_ms = [evs[q].elapsed_time(evs[q + 1]) for q in range(args.steps)]
+    elapsed = evs[0].elapsed_time(evs[-1])  # ms
+    t = torch.tensor([elapsed] + step_ms, dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed = float(t.item())
+    elapsed = float(t[0].item())
+    step_ms = [float(v) for v in t[1:].tolist()]
     ms_per = elapsed / args.steps
     fps = args.steps / (elapsed / 1000.0)
-    if pose_mode:
-        fps *= world  # every rank renders its own pose frames
+    per_fps = sorted(1000.0 / max(v, 1e-9) for v in step_ms)
+    pct = lambda p: per_fps[min(len(per_fps) - 1, int(round(p * (len(per_fps) - 1))))]  # noqa: E731
+    mult = world if pose_mode else 1  # every rank renders its own pose frames
+    fps *= mult
+    fps_dist = {"p10": pct(0.10) * mult, "median": pct(0.5) * mult, "p90": pct(0.90) * mult,
+                "unit": UNIT, "note": "per-step CUDA-event times (max over ranks per step)"}
+    launches = launches_per_step * args.steps
     clocks = clk.summary()
 
     # ---- e2e: public API with host buffers (rig H2D + frame D2H every step)
@@ -410,6 +408,24 @@ def main():
               "note": "traditional baseline: every view rendered full frame (own attributes, "
                       "RGB per pixel) then interlaced by V; same kernels' binning/sort"}
 
+    # ---- s = 4 beside the s = 8 headline: reuse is visibly lossy at s = 8 on
+    # this synthetic scene (profiles/r02/reuse_quality_config*.md), so the
+    # throughput of the next smaller cluster size is reported too (untimed loop)
+    s4 = None
+    if world == 1 and not pose_mode and cfg.cluster_size > 4:
+        for _ in range(2):
+            r.render(4, out=band_out)
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        fe0.record(stream)
+        n4 = 5
+        for _ in range(n4):
+            r.render(4, out=band_out)
+        fe1.record(stream)
+        torch.cuda.synchronize()
+        s4 = {"cluster_size": 4, "value": 1000.0 * n4 / fe0.elapsed_time(fe1), "unit": UNIT,
+              "frames": n4}
+
     # ---- ablation (stderr only)
     if args.ablation and rank == 0:
         for name, s_, rm, kn in [("ours s=8 staged", cfg.cluster_size, True, 0),
@@ -435,12 +451,14 @@ def main():
 
     peaks, peaks_src = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    comp_ms = ms_stage["composite"] / args.steps
+    comp_ms = ms_stage["composite"]
     evals = info["evals"]
     achieved_tflops = evals * FLOPS_PER_EVAL / (comp_ms * 1e-3) / 1e12 if comp_ms > 0 else None
     peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    # MUFU: 16 SFU lanes per SM (4 per SMSP) -> 148 x 16 x clock exponentials/s
+    mufu_peak = 148 * 16 * sm_max * 1e6 / 1e12
+    mufu_ach = evals * MUFU_PER_EVAL / (comp_ms * 1e-3) / 1e12 if comp_ms > 0 else None
     bc = compulsory_bytes(cfg, info) if world == 1 else None
-    traffic, ipc, traffic_src = committed_ncu("k_composite_staged")
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rows_s = (TY // 2 - args.ref_rows // 2, TY // 2 - args.ref_rows // 2 + args.ref_rows)
@@ -461,17 +479,21 @@ def main():
                    "output": "RGB8 interlaced frame in HBM"},
         "pairs": info["pairs"], "visible_ik": info["visible_ik"], "evals": evals,
         "mean_traversal": evals / max(1, band_out.numel()),  # rank 0's band
-        "stage_ms": {k: v / args.steps for k, v in ms_stage.items()},
+        "stage_ms": ms_stage,
+        "fps_distribution": fps_dist,
         "roofline": {"bound": "alu", "kernel": "k_composite_staged",
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     # the kernel is instruction-issue bound: issued IPC per SM of the
-                     # 4 schedulers (ncu sm__inst_executed.avg.per_cycle_active)
-                     "issue_ipc": ipc, "issue_frac": (ipc / 4.0) if ipc else None,
-                     "note": (f"{FLOPS_PER_EVAL} algorithmic FP32 ops per (subpixel, splat) "
-                              f"evaluation x {evals} evaluations / mean composite time; peak = "
-                              f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §5)")},
+                     "traffic": None,
+                     "mufu": {"achieved": mufu_ach, "peak": mufu_peak, "unit": "T exp/s",
+                              "frac": (mufu_ach / mufu_peak) if mufu_ach else None},
+                     "note": (f"{FLOPS_PER_EVAL} algorithmic FP32 ops + {MUFU_PER_EVAL} MUFU exp "
+                              f"per (subpixel, splat) evaluation (SURVEY §8d) x {evals} "
+                              "evaluations (the paper's traversal length, counted live by an "
+                              "instrumented frame) / the composite's CUDA-event time in this "
+                              f"run; peaks derived for {sm_max:.0f} MHz: 148 SM x 128 FP32 lanes "
+                              "x 2 and 148 SM x 16 SFU lanes (DESIGN.md §5); DRAM traffic per "
+                              "launch is not measured in this run (ncu captures: profiles/)")},
         "frame_hbm": ({"compulsory_bytes": bc, "achieved_gbs": bc / (ms_per * 1e-3) / 1e9,
                        "peak_gbs": peaks.get("hbm_gbs"), "peak_source": peaks_src,
                        "frac": bc / (ms_per * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
@@ -482,6 +504,11 @@ def main():
                 "note": "public API: cr_set_camera_rig from host + cr_render_interlaced into "
                         "pinned host memory (wall clock, max over ranks)"},
         "gpu_launches": launches,
+        "memory": {"peak_context_device_bytes": peak_ctx_bytes,
+                   "torch_max_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+                   "note": "the library's device buffers (grow-only: the context's peak) + "
+                           "torch's output / staging tensors"},
+        "reuse_s4": s4,
         "cpu_baseline": cpu,
         "fullframe_baseline": ff,
         "scene_gen_s": t_gen,

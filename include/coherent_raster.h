@@ -148,10 +148,17 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  *   flags          CR_FLAG_COUNT_EVALS counts (subpixel, splat) evaluations;
  *                  CR_FLAG_FULLFRAME renders the traditional baseline instead
  *                  (SURVEY N1): every one of the N views at full
- *                  resolution with its own attributes (cluster_size must be
- *                  1), one RGB pixel per thread, into an internal
- *                  [N][rows][W][3] buffer, then interlaced by V.
- *                  Equal, subpixel by subpixel, to the s=1 subpixel path.
+ *                  resolution with its own attributes (cluster_size 1), one
+ *                  RGB pixel per thread, into an internal [N][rows][W][3]
+ *                  buffer, then interlaced by V.  Equal, subpixel
+ *                  by subpixel, to the s=1 subpixel path.
+ *                  CR_FLAG_FULLFRAME with cluster_size s > 1 renders every view
+ *                  full frame with the attributes of its cluster (the per-view
+ *                  images of Cross-view Coherent Attribute Reuse the paper
+ *                  evaluates); interlaced it equals the subpixel path.
+ *                  CR_FLAG_VIEW_FRAMES (implies the full-frame render) returns
+ *                  those per-view frames instead of interlacing them: out is
+ *                  [N][rows][W][3], out_bytes >= N times the band size.
  * out: caller-owned, [rows][W][3] of the band (rows = clipped band height),
  * out_bytes must be >= rows*W*3*(1 or 4).  out_on_device selects a device
  * pointer (written on the stream) or a host pointer (copied back, the call
@@ -160,6 +167,7 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  * ------------------------------------------------------------------- */
 #define CR_FLAG_COUNT_EVALS 1
 #define CR_FLAG_FULLFRAME 2
+#define CR_FLAG_VIEW_FRAMES 4
 typedef struct {
   int32_t cluster_size;
   int32_t remap;

@@ -100,6 +100,7 @@ def _bind(L):
     sig("cro_get_image", None, vp, _f32p)
     sig("cro_get_records", None, vp, vp, vp, vp, vp, vp, vp)
     sig("cro_render_bruteforce", C.c_int, vp, _f32p)
+    sig("cro_render_views", C.c_int, vp, _f32p)
     return L
 
 
@@ -314,6 +315,13 @@ class Oracle:
         return dict(state=st.reshape(sh), depth=d.reshape(sh), cov2d=cv.reshape(sh + (4,)),
                     conic=cn.reshape(sh + (3,)), color=col.reshape(sh + (3,)),
                     count=cnt.reshape(sh))
+
+    def view_frames(self):
+        """Per-view frames [N, H, W, 3] of the last full-frame render."""
+        out = np.zeros((self.N, self.H, self.W, 3), np.float32)
+        if self._L.cro_render_views(self._c, out):
+            raise ValueError("cro_render_views needs a full-frame render")
+        return out
 
     def bruteforce(self):
         out = np.zeros((self.H, self.W, 3), np.float32)

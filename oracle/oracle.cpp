@@ -740,6 +740,45 @@ void cro_get_records(const cro_ctx* c, uint8_t* state, float* depth, float* cov2
     }
 }
 
+// Per-view frames of the last cro_render(s): every view j rendered full frame
+// (all pixels, all three channels) from its cluster's (t, k(j)) lists, per-view
+// means mu2D_{i,j} and the cluster's shared attributes — O12 applied to every
+// (j, x, y, u) instead of only u's view V[y][x][u] (the per-view images the
+// paper evaluates; Eq.4 then picks one view per subpixel).
+// dst: [N][H][W][3] float.  Requires a full-frame (row0 = 0, row1 = TY) render.
+int cro_render_views(cro_ctx* c, float* dst) {
+    const int64_t M = c->M;
+    const int N = c->N, W = c->W, H = c->H, s = c->s, TX = c->TX, K = c->K;
+    if (c->row0 != 0 || c->row1 != c->TY) return 1;
+    parallel_for((int64_t)N * H, c->nthreads, [&](int64_t jy) {
+        const int j = (int)(jy / H), y = (int)(jy % H);
+        const int k = j / s;
+        std::vector<Splat> L;
+        for (int x = 0; x < W; ++x) {
+            const size_t slot = (size_t)((y / 16) * TX + x / 16) * K + k;
+            for (int u = 0; u < 3; ++u) {
+                L.clear();
+                for (uint32_t e = c->S[slot]; e < c->E[slot]; ++e) {
+                    uint32_t i = c->pay[e];
+                    int64_t r = (int64_t)k * M + i;
+                    P3 pj = cam_point(c->cams[j], &c->means[3 * i]);
+                    if (pj.z < c->znear) continue;  // Z12
+                    Splat g;
+                    mean2d(c->cams[j], pj, &g.mx, &g.my);
+                    g.A = c->conA[r]; g.B = c->conB[r]; g.C = c->conC[r];
+                    g.o = c->opac[i];
+                    g.col = c->col[3 * r + u];
+                    L.push_back(g);
+                }
+                dst[(((size_t)j * H + y) * W + x) * 3 + u] =
+                    blend(L.data(), (int)L.size(), (float)x + 0.5f, (float)y + 0.5f, c->bg[u],
+                          nullptr);
+            }
+        }
+    });
+    return 0;
+}
+
 // Brute force (north_star check): render every view full frame with no
 // tiles — per pixel all Gaussians with (i, k(j)) not culled and visible from
 // v_j, ordered by (d_{i,k(j)}, i) — then interlace by V.

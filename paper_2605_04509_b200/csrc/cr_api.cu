@@ -630,9 +630,8 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (o->kernel == 0 && o->remap == 0)
     return fail(c, CR_ERR_INVALID_ARG, "the staged composite needs remap=1 (use kernel=1)");
   if (o->output_format != 0 && o->output_format != 1) return fail(c, CR_ERR_INVALID_ARG, "format");
-  const bool fullframe = (o->flags & CR_FLAG_FULLFRAME) != 0;
-  if (fullframe && s != 1)
-    return fail(c, CR_ERR_INVALID_CONFIG, "the full-frame baseline renders every view: cluster_size must be 1");
+  const bool view_frames = (o->flags & CR_FLAG_VIEW_FRAMES) != 0;
+  const bool fullframe = view_frames || (o->flags & CR_FLAG_FULLFRAME) != 0;
   for (int u = 0; u < 3; ++u)
     if (!std::isfinite(o->background[u])) return fail(c, CR_ERR_NONFINITE, "background");
   int row0 = o->tile_row_begin, row1 = o->tile_row_end;
@@ -640,7 +639,8 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (row0 < 0 || row1 > TY || row0 >= row1)
     return fail(c, CR_ERR_INVALID_ARG, "tile rows [%d,%d) outside [0,%d)", row0, row1, TY);
   const int y0 = row0 * 16, y1 = std::min(H, row1 * 16);
-  const size_t obytes = (size_t)(y1 - y0) * W * 3 * (o->output_format ? 4 : 1);
+  const size_t obytes =
+      (size_t)(y1 - y0) * W * 3 * (o->output_format ? 4 : 1) * (view_frames ? (size_t)N : 1);
   if (out_bytes < obytes) return fail(c, CR_ERR_INVALID_ARG, "out_bytes %zu < %zu", out_bytes, obytes);
   // O3 clusters
   const int K = (N + s - 1) / s;
@@ -991,20 +991,27 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
   const int fmt = o->output_format;
   if (fullframe) {
-    const size_t fb = (size_t)N * (y1 - y0) * W * 3 * (fmt ? 4 : 1);
-    CR_TRY(ensure(c, c->frames, fb));
+    // per-view frames [N][rows][W][3]: straight into the caller's buffer for
+    // CR_FLAG_VIEW_FRAMES (no interlace), else into the context's buffer
+    void* fr = dst;
+    if (!view_frames) {
+      const size_t fb = (size_t)N * (y1 - y0) * W * 3 * (fmt ? 4 : 1);
+      CR_TRY(ensure(c, c->frames, fb));
+      fr = c->frames.p;
+    }
     const unsigned nb = ntile * (unsigned)N;
     if (fmt == 0)
       k_fullframe<0><<<nb, 256, 0, str>>>(P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,
-                                          P_<float4>(c->rec0), m4, c->frames.p);
+                                          P_<float4>(c->rec0), m4, fr);
     else
       k_fullframe<1><<<nb, 256, 0, str>>>(P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,
-                                          P_<float4>(c->rec0), m4, c->frames.p);
-    CR_LAUNCHED(c);
-    const long long nsub = (long long)(y1 - y0) * W * 3;
-    const unsigned gi = (unsigned)std::min<long long>(grid_for(nsub, 256), 148 * 32);
-    if (fmt == 0) k_interlace<0><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
-    else k_interlace<1><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
+                                          P_<float4>(c->rec0), m4, fr);
+    if (!view_frames) {
+      const long long nsub = (long long)(y1 - y0) * W * 3;
+      const unsigned gi = (unsigned)std::min<long long>(grid_for(nsub, 256), 148 * 32);
+      if (fmt == 0) k_interlace<0><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
+      else k_interlace<1><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), c->frames.p, dst, y1 - y0);
+    }
   } else if (o->kernel == 0) {
     if (fmt == 0) { if (count) CR_STAGED(0, true); else CR_STAGED(0, false); }
     else          { if (count) CR_STAGED(1, true); else CR_STAGED(1, false); }

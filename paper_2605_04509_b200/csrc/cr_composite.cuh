@@ -309,12 +309,15 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
 }
 
 // ===========================================================================
-// N1 baseline: full-frame 3DGS of every view, then interlace.
+// Full-frame render of every view, then interlace.
 // CTA = (tile, view j): 256 threads = the tile's pixels, RGB per thread; list
-// (t, j) of the s=1 binning; entries staged in shared memory 256 at a time
-// with their view-j mean; a CTA-wide count ends the list when all pixels
-// saturate.  Each channel uses exactly the staged kernel's blend arithmetic,
-// so interlacing the frames reproduces the s=1 subpixel render bit for bit.
+// (t, k(j)) of the binning at cluster size s (s = 1: the traditional N1
+// baseline, each view with its own attributes; s > 1: the per-view images of
+// Cross-view Coherent Attribute Reuse that the paper evaluates);
+// entries staged in shared memory 256 at a time with their view-j mean; a
+// CTA-wide count ends the list when all pixels saturate.  Each channel uses
+// exactly the staged kernel's blend arithmetic, so interlacing the frames
+// reproduces the subpixel render at the same s bit for bit.
 // ===========================================================================
 template <int FMT>
 __global__ void __launch_bounds__(256) k_fullframe(const uint32_t* __restrict__ S,
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(256) k_fullframe(const uint32_t* __restrict__ 
   const int x = tx * 16 + (threadIdx.x & 15), y = ty * 16 + (threadIdx.x >> 4);
   const bool inside = x < W && y < H;
   const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-  const int k = j;  // s = 1: every view is its own cluster
+  const int k = j / c_fp.s;  // GetClusterID(j)
   const uint32_t e0 = S[t * K + k], e1 = E[t * K + k];
   const long long kM = (long long)k * M;
   const CamDev& cam = c_cams[j];

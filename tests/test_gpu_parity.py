@@ -350,9 +350,10 @@ def test_fullframe_baseline_equals_subpixel_s1(cfgA_pair):
     assert np.abs(ff - bf).max() <= 2.0 / 255 and psnr(np.clip(ff, 0, 1), np.clip(bf, 0, 1)) >= 50
     band = g.render(1, output_format="rgb8", fullframe=True, rows=(2, 6)).cpu().numpy()
     assert np.array_equal(band, g.render(1, output_format="rgb8", rows=(2, 6)).cpu().numpy())
-    from paper_2605_04509_b200._native import CrError
-    with pytest.raises(CrError, match="INVALID_CONFIG"):
-        g.render(8, fullframe=True)
+    # s > 1: every view full frame with its cluster's attributes, interlaced ==
+    # the subpixel path at the same s (same lists, means and blend arithmetic)
+    assert np.array_equal(g.render(4, output_format="float", fullframe=True).cpu().numpy(),
+                          g.render(4, output_format="float").cpu().numpy())
 
 
 @pytest.mark.parametrize("s", [16, 18, 3])
