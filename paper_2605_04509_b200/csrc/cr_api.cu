@@ -138,6 +138,7 @@ struct cr_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
+  int exp = 0;         // CR_EXP (read once at cr_create): developer A/B switches, 0 = shipped path
   bool motion_bound = false;  // pre-cull by the cluster motion bound (narrow clusters)
 };
 
@@ -411,6 +412,8 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
   c->device = cuda_device;
   const char* dbg = getenv("CR_DEBUG");
   c->debug = dbg && dbg[0] && dbg[0] != '0';
+  const char* ex = getenv("CR_EXP");
+  c->exp = ex ? atoi(ex) : 0;
   if (c->debug) {
     signal(SIGSEGV, segv_handler);
     signal(SIGBUS, segv_handler);
@@ -662,6 +665,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   fp.W = W; fp.H = H; fp.TX = TX; fp.TY = TY; fp.N = N; fp.s = s; fp.K = K; fp.bitK = bitK;
   fp.row0 = row0; fp.row1 = row1; fp.deg = c->deg; fp.remap = o->remap; fp.M = M;
   fp.divM = make_fastdiv((uint32_t)std::max<long long>(M, 1));
+  fp.exp = c->exp;
   fp.znear = c->znear;
   for (int u = 0; u < 3; ++u) fp.bg[u] = o->background[u];
   std::vector<int> rep(K);

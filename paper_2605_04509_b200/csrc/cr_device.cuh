@@ -56,6 +56,7 @@ struct FrameParams {
   FastDiv divM;  // record r = k*M + i  ->  k = fdiv(r, divM)
   float znear;
   float bg[3];
+  int exp;  // CR_EXP developer A/B switches (0 = shipped path)
 };
 
 __constant__ CamDev c_cams[kMaxViews];

@@ -1,9 +1,10 @@
 """Row-band sharding of the interlaced frame over the GPUs of one node
 (SURVEY §8(e)).  Gaussians are replicated; rank r renders tile rows
 band_rows(TY, R, r) of the frame (keys keep global tile ids, so its pairs are
-the full frame's pairs filtered to the band); the RGB8 bands are padded to a
-common height and assembled with one all_gather_into_tensor (NCCL over
-NVLink on B200, gloo in the CPU tests).  Pose batches (config E) split the
+the full frame's pairs filtered to the band); every rank renders straight into
+its rows of a full-frame buffer and the bands are exchanged in place with one
+broadcast per band (NCCL over NVLink on B200, gloo in the CPU tests) — no
+padding to the tallest band.  Pose batches (config E) split the
 poses round-robin with no collective.
 """
 from __future__ import annotations
@@ -72,52 +73,42 @@ def band_pixel_rows(H: int, TY: int, world: int, rank: int, bands=None):
     return _pix(H, r0, r1)
 
 
-def padded_band_height(H: int, TY: int, world: int, bands=None) -> int:
-    return max(band_pixel_rows(H, TY, world, q, bands)[1] - band_pixel_rows(H, TY, world, q, bands)[0]
-               for q in range(world))
-
-
-def assemble(gathered: torch.Tensor, H: int, TY: int, world: int, bands=None) -> torch.Tensor:
-    """Full frame [H, W, 3] from the all-gathered padded bands [world*hp, W, 3]."""
-    hp = gathered.shape[0] // world
-    parts = []
-    for q in range(world):
-        y0, y1 = band_pixel_rows(H, TY, world, q, bands)
-        parts.append(gathered[q * hp:q * hp + (y1 - y0)])
-    return torch.cat(parts, 0)
-
-
 class BandGather:
-    """Preallocated padded band buffer + gather target for one rank."""
+    """Full-frame buffer of one rank; the rank renders its band straight into
+    its rows (row-major, so the band is a contiguous slice) and gather()
+    fills the other ranks' rows in place with one broadcast per band (NCCL
+    over NVLink): every rank receives exactly the frame's other rows — no
+    padding to the tallest band (balanced bands differ in height)."""
 
     def __init__(self, H: int, W: int, TY: int, world: int, rank: int, device, dtype=torch.uint8,
                  bands=None):
         self.H, self.W, self.TY, self.world, self.rank = H, W, TY, world, rank
         self.bands = bands
         self.rows = bands[rank] if bands else band_rows(TY, world, rank)
-        y0, y1 = band_pixel_rows(H, TY, world, rank, bands)
-        self.hp = padded_band_height(H, TY, world, bands)
-        self.band = torch.zeros((self.hp, W, 3), dtype=dtype, device=device)
-        self.out = self.band[:y1 - y0]  # what the renderer writes
-        self.full = (torch.empty((world * self.hp, W, 3), dtype=dtype, device=device)
-                     if world > 1 else None)
+        self.full = torch.zeros((H, W, 3), dtype=dtype, device=device)
+        self.pix = [band_pixel_rows(H, TY, world, q, bands) for q in range(world)]
+        y0, y1 = self.pix[rank]
+        self.out = self.full[y0:y1]  # what the renderer writes (contiguous rows)
 
     def gather(self, group=None) -> torch.Tensor:
-        """All-gather the padded bands; returns the padded stack (or the band at world 1)."""
+        """Fill every other rank's band rows; returns the full frame."""
         if self.world == 1:
-            return self.band
-        if dist.get_backend(group) == "nccl" or self.band.device.type == "cpu":
-            dist.all_gather_into_tensor(self.full, self.band, group=group)
-        else:  # gloo with CUDA tensors (tests): list all_gather through host copies
-            parts = [torch.empty_like(self.band, device="cpu") for _ in range(self.world)]
-            dist.all_gather(parts, self.band.cpu(), group=group)
-            self.full.copy_(torch.cat(parts, 0))
+            return self.full
+        on_host = dist.get_backend(group) != "nccl" and self.full.device.type != "cpu"
+        buf = self.full.cpu() if on_host else self.full  # gloo with CUDA tensors (tests)
+        for q, (y0, y1) in enumerate(self.pix):
+            if y1 > y0:
+                dist.broadcast(buf[y0:y1], src=q, group=group)
+        if on_host:
+            self.full.copy_(buf)
         return self.full
 
     def frame(self) -> torch.Tensor:
-        if self.world == 1:
-            return self.out
-        return assemble(self.full, self.H, self.TY, self.world, self.bands)
+        return self.full
+
+    def bytes_received(self) -> int:
+        y0, y1 = self.pix[self.rank]
+        return (self.H - (y1 - y0)) * self.W * 3 * self.full.element_size()
 
 
 def row_pair_weights(renderer, cluster_size: int):

@@ -94,7 +94,9 @@ def _worker(rank, world, port, H, W, q, balanced=False):
     bg.out.copy_(torch.from_numpy(ref[y0:y1]))  # "render" this rank's band
     bg.gather()
     full = bg.frame().numpy()
-    q.put((rank, bool(np.array_equal(full, ref)), bg.rows))
+    # unpadded: each rank receives exactly the other ranks' rows
+    q.put((rank, bool(np.array_equal(full, ref)) and bg.bytes_received() == (H - (y1 - y0)) * W * 3,
+           bg.rows))
     dist.barrier()
     dist.destroy_process_group()
 
