@@ -984,11 +984,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   const float4* m4 = P_<float4>(c->mean4);
   const bool count = (o->flags & CR_FLAG_COUNT_EVALS) != 0;
   unsigned long long* evals = counters + 3;
-#define CR_STAGED(F, CNT)                                                                     \
-  k_composite_staged<F, CNT, kCompWarps, 0><<<ntile, kCompWarps * 32, 0, str>>>(             \
+#define CR_STAGED1(F, CNT, VAR)                                                                \
+  k_composite_staged<F, CNT, kCompWarps, VAR><<<ntile, kCompWarps * 32, 0, str>>>(           \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
       P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
+#define CR_STAGED(F, CNT) CR_STAGED1(F, CNT, 0)
 #define CR_THREAD(F, CNT)                                                                     \
   k_composite_thread<F, CNT><<<ntile, kTileSub, 0, str>>>(                                    \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,    \
@@ -1024,6 +1025,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     else          { if (count) CR_THREAD(1, true); else CR_THREAD(1, false); }
   }
 #undef CR_STAGED
+#undef CR_STAGED1
 #undef CR_THREAD
   CR_LAUNCHED(c);
   CR_TRACE(c, "composite");

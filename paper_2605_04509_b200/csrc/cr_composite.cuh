@@ -13,7 +13,7 @@
 //   P:379-382, and skipping them is exact).  Every lane then walks only its
 //   view's surviving entries from shared memory (broadcast reads).  A warp
 //   ballot ends the list as soon as every lane has saturated.  Results go to
-//   a smem tile and leave in coalesced row stores.
+//   a smem tile and leave in 16-byte vector row stores (store_tile).
 // k_composite_thread (the paper's design): one thread per subpixel rank r,
 //   x = Psi(r) (remap=1) or raster order (remap=0), private list traversal
 //   with direct gathers and a direct scattered store.
@@ -93,19 +93,53 @@ __device__ __forceinline__ void blend_step(const float4 g, const float2 m, const
   }
 }
 
+// RGB8 quantisation: floor(min(max(v,0),1) * 255 + 1/2), fp32
+__device__ __forceinline__ uint32_t quant_u8(float v) {
+  const float cl = fminf(fmaxf(v, 0.0f), 1.0f);
+  return (uint32_t)floorf(__fadd_rn(__fmul_rn(cl, 255.0f), 0.5f));
+}
+
+// Interlaced tile out of shared memory.  A full 16-pixel-wide tile row is
+// 48 bytes (RGB8) or 192 bytes (float) starting at a multiple of 48 / 192
+// bytes within its image row, so when the image row pitch W*3 (bytes, RGB8)
+// is a multiple of 16 every tile row leaves in 16-byte vector stores: 3 x
+// uint4 of 16 quantised subpixels (RGB8) or 12 x float4 (float) per row.
+// Partial tiles (right frame edge), unaligned pitches or buffers store
+// subpixel by subpixel.
 template <int FMT>
 __device__ __forceinline__ void store_tile(const float* s_out, void* out, int tx, int ty, int W,
                                            int H, int y_band0) {
   const int nx = min(16, W - tx * 16), ny = min(16, H - ty * 16);
+  if (nx == 16 && (W * 3) % 16 == 0 && ((uintptr_t)out & 15) == 0) {
+    constexpr int kVecRow = FMT == 0 ? 3 : 12;  // 16-byte vectors per tile row
+    for (int q = threadIdx.x; q < ny * kVecRow; q += blockDim.x) {
+      const int ly = q / kVecRow, part = q % kVecRow;
+      const long long row = (long long)(ty * 16 + ly - y_band0) * W + tx * 16;
+      if (FMT == 0) {
+        const float4* src = reinterpret_cast<const float4*>(s_out + ly * 48 + part * 16);
+        uint32_t wd[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float4 f = src[v];
+          wd[v] = quant_u8(f.x) | (quant_u8(f.y) << 8) | (quant_u8(f.z) << 16) |
+                  (quant_u8(f.w) << 24);
+        }
+        reinterpret_cast<uint4*>((uint8_t*)out + row * 3)[part] =
+            make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      } else {
+        reinterpret_cast<float4*>((float*)out + row * 3)[part] =
+            reinterpret_cast<const float4*>(s_out + ly * 48)[part];
+      }
+    }
+    return;
+  }
   if (FMT == 0) {
     uint8_t* o = (uint8_t*)out;
     const int rowb = nx * 3;
     for (int q = threadIdx.x; q < ny * rowb; q += blockDim.x) {
       const int ly = q / rowb, b = q % rowb;
-      const float v = s_out[ly * 48 + b];
-      const float cl = fminf(fmaxf(v, 0.0f), 1.0f);
-      const uint8_t u8 = (uint8_t)floorf(__fadd_rn(__fmul_rn(cl, 255.0f), 0.5f));
-      o[((long long)(ty * 16 + ly - y_band0) * W + tx * 16) * 3 + b] = u8;
+      o[((long long)(ty * 16 + ly - y_band0) * W + tx * 16) * 3 + b] =
+          (uint8_t)quant_u8(s_out[ly * 48 + b]);
     }
   } else {
     float* o = (float*)out;
@@ -161,7 +195,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
   __shared__ float2 s_mu[NW][kSlots][32];
   __shared__ float4 s_box[NW][kSlots];  // per staged view: pixel box centre, half size
   __shared__ float4 s_cam4[NW][kSlots][4];  // per staged view: camera (4 float4)
-  __shared__ float s_out[kTileSub];
+  __shared__ __align__(16) float s_out[kTileSub];
   __shared__ int s_next;
   const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
   const long long M = c_fp.M;
