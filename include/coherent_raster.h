@@ -49,10 +49,7 @@ typedef enum {
   CR_ERR_NOT_READY = 6,        /* render before upload/display/rig          */
   CR_ERR_OUT_OF_MEMORY = 7,    /* device allocation failed                   */
   CR_ERR_CUDA = 8,             /* any other CUDA runtime error               */
-  CR_ERR_CAPACITY = 9,         /* pair / row-entry count exceeds 2^32 - 1,
-                                  or a device store could not be grown      */
-  CR_ERR_INTERNAL = 10         /* a device-side consistency check failed
-                                  (a library bug; the frame is not valid)   */
+  CR_ERR_CAPACITY = 9          /* pair count exceeds 2^32 - 1               */
 } cr_status;
 
 /* Create a context on `cuda_device`.  `cuda_stream` is a cudaStream_t (may be

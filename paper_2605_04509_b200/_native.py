@@ -14,7 +14,7 @@ from .build import LIB
 STATUS = {
     0: "CR_OK", 1: "CR_ERR_INVALID_ARG", 2: "CR_ERR_INVALID_CONFIG", 3: "CR_ERR_CONFIG_MISMATCH",
     4: "CR_ERR_TILE_ID_OVERFLOW", 5: "CR_ERR_NONFINITE", 6: "CR_ERR_NOT_READY",
-    7: "CR_ERR_OUT_OF_MEMORY", 8: "CR_ERR_CUDA", 9: "CR_ERR_CAPACITY", 10: "CR_ERR_INTERNAL",
+    7: "CR_ERR_OUT_OF_MEMORY", 8: "CR_ERR_CUDA", 9: "CR_ERR_CAPACITY",
 }
 
 # exported symbols, in header order (tests check the library exports all of them)

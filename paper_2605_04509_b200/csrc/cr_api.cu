@@ -32,7 +32,6 @@
 #include "cr_device.cuh"
 #include "cr_kernels.cuh"
 #include "cr_sort.cuh"
-#include "cr_rowbin.cuh"
 
 #ifndef CR_GIT_TAG
 #define CR_GIT_TAG "dev"
@@ -123,13 +122,6 @@ struct cr_ctx {
   DevBuf hist, scalars, S, E, stage_out, frames;
   DevBuf look;                     // onesweep look-back status words
   DevBuf slook;                    // single-pass scan look-back status words + ticket
-  // row-bucketed binning tail (cr_rowbin.cuh): per-row histograms [2][512],
-  // k_rowbin tile -> first record, row-bucketed entries, entry pair offsets,
-  // k_colsort tile -> first entry, per-tile pair counts / list bases, the
-  // big-record entry store (+ [0] allocation counter, [1..2] error flags)
-  DevBuf rowhist, tfirst, rbent, rbpoff, rbcmap, tilehist, tilebase, bigent, bigctl;
-  bool rb_frame = false;           // the last frame took the row-bucketed tail
-  DevBuf slotkeys;                 // introspection: (t, k) slot per sorted pair (RB frames)
   uint32_t sepoch = 0;
   uint32_t epoch = 0;              // look-back tag of the last radix pass
   DevBuf tmp;                      // upload staging
@@ -236,9 +228,14 @@ T* P_(DevBuf& b) { return (T*)b.p; }
 
 unsigned grid_for(long long n, int block) { return (unsigned)((n + block - 1) / block); }
 
-// Look-back state of a single-pass scan over nb tiles (k_scan_onepass,
-// k_rowscan): zeroed ticket + status words tagged with a fresh epoch.
-cr_status scan_lookback(cr_ctx* c, long long nb, uint32_t** ticket, unsigned long long** look) {
+// device exclusive scan: out(i, excl, in(i)); *d_total = sum
+template <class In, class Out>
+cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
+  if (n <= 0) {
+    CR_CUDA(c, cudaMemsetAsync(d_total, 0, 4, c->stream));
+    return CR_OK;
+  }
+  const long long nb = (n + kScanTile - 1) / kScanTile;
   const size_t lbytes = (size_t)nb * 8 + 64;  // the ticket counter + status words
   if (lbytes > c->slook.bytes || !c->slook.p) {
     CR_TRY(ensure(c, c->slook, lbytes));
@@ -249,23 +246,9 @@ cr_status scan_lookback(cr_ctx* c, long long nb, uint32_t** ticket, unsigned lon
     CR_CUDA(c, cudaMemsetAsync(c->slook.p, 0, c->slook.bytes, c->stream));
     c->sepoch = 1;
   }
-  *ticket = P_<uint32_t>(c->slook);  // first 64 bytes: ticket; then status words
-  *look = (unsigned long long*)((char*)c->slook.p + 64);
-  CR_CUDA(c, cudaMemsetAsync(*ticket, 0, 4, c->stream));
-  return CR_OK;
-}
-
-// device exclusive scan: out(i, excl, in(i)); *d_total = sum
-template <class In, class Out>
-cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
-  if (n <= 0) {
-    CR_CUDA(c, cudaMemsetAsync(d_total, 0, 4, c->stream));
-    return CR_OK;
-  }
-  const long long nb = (n + kScanTile - 1) / kScanTile;
-  uint32_t* ticket = nullptr;
-  unsigned long long* look = nullptr;
-  CR_TRY(scan_lookback(c, nb, &ticket, &look));
+  uint32_t* ticket = P_<uint32_t>(c->slook);  // first 64 bytes: ticket; then status words
+  unsigned long long* look = (unsigned long long*)((char*)c->slook.p + 64);
+  CR_CUDA(c, cudaMemsetAsync(ticket, 0, 4, c->stream));
   int* ovf = P_<int>(c->scalars) + 3;
   k_scan_onepass<In, Out><<<(unsigned)nb, kScanThreads, 0, c->stream>>>(in, out, n, look, ticket,
                                                                          c->sepoch, d_total, ovf);
@@ -413,7 +396,6 @@ const char* cr_status_string(cr_status s) {
     case CR_ERR_OUT_OF_MEMORY: return "CR_ERR_OUT_OF_MEMORY";
     case CR_ERR_CUDA: return "CR_ERR_CUDA";
     case CR_ERR_CAPACITY: return "CR_ERR_CAPACITY";
-    case CR_ERR_INTERNAL: return "CR_ERR_INTERNAL";
   }
   return "CR_ERR_UNKNOWN";
 }
@@ -437,7 +419,7 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
     signal(SIGBUS, segv_handler);
   }
   c->stream = (cudaStream_t)cuda_stream;
-  if (cudaSetDevice(cuda_device) != cudaSuccess || cudaMallocHost(&c->h_pinned, 8192) != cudaSuccess) {
+  if (cudaSetDevice(cuda_device) != cudaSuccess || cudaMallocHost(&c->h_pinned, 256) != cudaSuccess) {
     delete c;
     return CR_ERR_CUDA;
   }
@@ -461,9 +443,7 @@ void cr_destroy(cr_ctx* c) {
                    &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->bigcnt,
                    &c->bigmask, &c->bigwlo, &c->biginfo, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->hist, &c->look, &c->slook,
-                   &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp,
-                   &c->rowhist, &c->tfirst, &c->rbent, &c->rbpoff, &c->rbcmap, &c->tilehist,
-                   &c->tilebase, &c->bigent, &c->bigctl, &c->slotkeys};
+                   &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -873,229 +853,46 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRACE(c, "depth presort");
   CR_CUDA(c, cudaEventRecord(c->ev[2], str));
 
-  // ---- a6 count (+ offsets and emission, or the row-bucketed tail), a7 tile
-  // sort, a8 ranges
+  // ---- a6 offsets + emit
   uint32_t P = 0;
   int tbits = 1;
   while ((1LL << tbits) < (long long)TX * TY) ++tbits;
   const int tpass = (tbits + 7) / 8;
-  const int nbr = row1 - row0;
-  // row-bucketed tail (cr_rowbin.cuh) for bands of <= 512 tile rows on frames
-  // of <= 512 tile columns; CR_EXP bit 3 forces emission + LSD (A/B, tests)
-  const bool rb = nbr <= kRbMaxRows && TX <= kRbMaxRows && !(c->exp & 8);
-  c->rb_frame = rb;
-  // count in (k, depth, i) order: position-indexed counts and union slots
-  // k_countv: 16 blocks per resident slot, so the grid-stride tail is short
-  // (measured at config C: binning 6.38 ms at 148 x 8 blocks, 6.27 at x16,
-  // 6.20 at x32, 6.14 at x64, 6.18 at x128); small frames: no more blocks
-  // than 64-record blocks of work
-  const unsigned count_grid =
-      (unsigned)std::min<long long>(148 * 64, std::max<long long>(148, ((long long)nvis + 63) / 64));
-  uint32_t* rowhist = nullptr;
-  BigEnt bigent{};
-  if (rb) {
-    CR_TRY(ensure(c, c->rowhist, (2 * kRbMaxRows + 3 * kRowTab) * 4));
-    CR_TRY(ensure(c, c->bigctl, 64));
-    // big-record entries (CR_EXP bit 4: start from 64 so tests exercise the grow-and-redo path)
-    const size_t bcapE = (c->exp & 16) ? 64 : std::max<size_t>(1 << 16, Rz / 4);
-    if (c->bigent.bytes < bcapE * 16) CR_TRY(ensure(c, c->bigent, bcapE * 16));
-    rowhist = P_<uint32_t>(c->rowhist);
-    bigent = BigEnt{P_<uint4>(c->bigent), P_<uint32_t>(c->bigctl),
-                    (uint32_t)std::min<size_t>(c->bigent.bytes / 16, 0xFFFFFFFFu),
-                    P_<uint32_t>(c->bigctl) + 1};
-  }
-  auto launch_counts = [&]() -> cr_status {
-    // cameras (N x 80 B) are dynamic shared memory on top of the static arrays
-#define CR_DYN(KERN) cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cam_smem)
-#define CR_COUNTS(GG, RBV)                                                                         \
-  CR_DYN((k_countv<8, 3, RBV>));                                                              \
-  CR_DYN((k_countv<(GG >= 8 ? GG / 2 : 1), 2, RBV>));                                          \
-  CR_DYN((k_countv<GG, 1, RBV>));                                                             \
-  CR_DYN(k_count_big_rb<GG>);                                                                 \
-  CR_DYN(k_count_big<GG>);                                                                    \
+  if (nvis > 0) {
+    // count in (k, depth, i) order: position-indexed counts and union slots
+    // k_countv: 16 blocks per resident slot, so the grid-stride tail is short
+    // (measured at config C: binning 6.38 ms at 148 x 8 blocks, 6.27 at x16,
+    // 6.20 at x32, 6.14 at x64, 6.18 at x128); small frames: no more blocks
+    // than 64-record blocks of work
+    const unsigned count_grid =
+        (unsigned)std::min<long long>(148 * 64, std::max<long long>(148, ((long long)nvis + 63) / 64));
+#define CR_COUNTS(GG)                                                                         \
   if (GG == 32 && s <= 24) /* 17..24 views: three per lane, 8-lane groups (P4K s=18:      \
                                 binning 9.2 -> 8.3 ms vs 16 lanes x 2 views) */              \
-    k_countv<8, 3, RBV><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
+    k_countv<8, 3><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6, rowhist);                               \
+        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
   else if (GG >= 8) /* two views per lane */                                                  \
-    k_countv<(GG >= 8 ? GG / 2 : 1), 2, RBV><<<count_grid, kBinThreads, cam_smem, str>>>(          \
+    k_countv<(GG >= 8 ? GG / 2 : 1), 2><<<count_grid, kBinThreads, cam_smem, str>>>(          \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6, rowhist);                               \
+        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
   else                                                                                        \
-    k_countv<GG, 1, RBV><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
+    k_countv<GG, 1><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6, rowhist);                               \
+        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
   CR_LAUNCHED(c);                                                                             \
-  if (RBV)                                                                                    \
-    k_count_big_rb<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                              \
-        P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
-        P_<uint32_t>(c->cnt), P_<uint4>(c->slots), bigent, rowhist);                          \
-  else                                                                                        \
-    k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                 \
-        P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
-        P_<uint32_t>(c->cnt), bigrows)
-    if (rb) {
-      switch (G) {
-        case 1: CR_COUNTS(1, true); break;
-        case 2: CR_COUNTS(2, true); break;
-        case 4: CR_COUNTS(4, true); break;
-        case 8: CR_COUNTS(8, true); break;
-        case 16: CR_COUNTS(16, true); break;
-        default: CR_COUNTS(32, true); break;
-      }
-    } else {
-      switch (G) {
-        case 1: CR_COUNTS(1, false); break;
-        case 2: CR_COUNTS(2, false); break;
-        case 4: CR_COUNTS(4, false); break;
-        case 8: CR_COUNTS(8, false); break;
-        case 16: CR_COUNTS(16, false); break;
-        default: CR_COUNTS(32, false); break;
-      }
+  k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                   \
+      P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
+      P_<uint32_t>(c->cnt), bigrows)
+    switch (G) {
+      case 1: CR_COUNTS(1); break;
+      case 2: CR_COUNTS(2); break;
+      case 4: CR_COUNTS(4); break;
+      case 8: CR_COUNTS(8); break;
+      case 16: CR_COUNTS(16); break;
+      default: CR_COUNTS(32); break;
     }
 #undef CR_COUNTS
-#undef CR_DYN
-    return CR_OK;
-  };
-  uint32_t *tA = nullptr, *pA = nullptr;
-  if (rb) {
-    // ---- count -> row entries (k_countv / k_count_big_rb), entry offsets,
-    // row-bucketed entries (k_rowbin), pair offsets + tile histogram
-    // (k_rowscan), list bases (k_tile_bases), column sort (k_colsort), ranges
-    uint32_t NE = 0;
-    for (int attempt = 0;; ++attempt) {
-      CR_CUDA(c, cudaMemsetAsync(c->rowhist.p, 0, 2 * kRbMaxRows * 4, str));
-      CR_CUDA(c, cudaMemsetAsync(c->bigctl.p, 0, 16, str));
-      CR_CUDA(c, cudaMemsetAsync(sc + 1, 0, 4 * 6, str));  // totals, overflow, big-record count
-      const uint32_t ntB_cap = (uint32_t)(((size_t)nvis * kSlotRows + bigent.cap) / kRbTE + 2);
-      CR_TRY(ensure(c, c->tfirst, (size_t)ntB_cap * 4));
-      if (nvis > 0) {
-        CR_TRY(launch_counts());
-        CR_LAUNCHED(c);
-        CR_TRACE(c, "count");
-        CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->cnt)},
-                        OutEoff{P_<uint32_t>(c->offs), P_<uint32_t>(c->tfirst)}, nvis, sc + 1));
-      } else {
-        CR_CUDA(c, cudaMemsetAsync(sc + 1, 0, 4, str));
-      }
-      // one read: entry total, the band's per-row entry / pair counts, big-store flags
-      CR_CUDA(c, cudaMemcpyAsync(c->h_pinned, sc, 16, cudaMemcpyDeviceToHost, str));
-      CR_CUDA(c, cudaMemcpyAsync(c->h_pinned + 4, c->bigctl.p, 16, cudaMemcpyDeviceToHost, str));
-      CR_CUDA(c, cudaMemcpyAsync(c->h_pinned + 8, c->rowhist.p, 2 * kRbMaxRows * 4,
-                                 cudaMemcpyDeviceToHost, str));
-      CR_CUDA(c, cudaStreamSynchronize(str));
-      const uint32_t* hp = c->h_pinned;
-      if (hp[5] && attempt == 0) {  // big-record store too small: grow to the demand, redo
-        CR_TRY(ensure(c, c->bigent, ((size_t)hp[4] + hp[4] / 4 + 1024) * 16));
-        bigent.e = P_<uint4>(c->bigent);
-        bigent.cap = (uint32_t)std::min<size_t>(c->bigent.bytes / 16, 0xFFFFFFFFu);
-        continue;
-      }
-      if (hp[5]) return fail(c, CR_ERR_CAPACITY, "big-record entry store (%u entries)", hp[4]);
-      if (hp[6]) return fail(c, CR_ERR_INTERNAL, "big-record column window");
-      if (hp[3]) return fail(c, CR_ERR_CAPACITY, "row entry count exceeds 2^32-1");
-      NE = hp[1];
-      unsigned long long sumE = 0, sumP = 0;
-      for (int q = 0; q < nbr; ++q) {
-        sumE += hp[8 + q];
-        sumP += hp[8 + kRbMaxRows + q];
-      }
-      if (sumE != NE) return fail(c, CR_ERR_INTERNAL, "row entries %llu != %u", sumE, NE);
-      if (sumP > 0xFFFFFFFFull) return fail(c, CR_ERR_CAPACITY, "pair count exceeds 2^32-1");
-      P = (uint32_t)sumP;
-      break;
-    }
-    unsigned long long ntC = 0;
-    for (int q = 0; q < nbr; ++q) ntC += (c->h_pinned[8 + kRbMaxRows + q] + kRbTP - 1) / kRbTP;
-    const uint32_t ntB = (NE + kRbTE - 1) / kRbTE;
-    const bool wide = nbr > 256 || TX > 256;  // 9-bit digits
-    const int ndB = nbr > 256 ? 512 : 256, ndC = wide ? 512 : 256;
-    const size_t NEz = std::max<size_t>(NE, 1), Pz = std::max<size_t>(P, 1);
-    const size_t ntile_b = (size_t)nbr * TX;
-    CR_TRY(ensure(c, c->rbent, NEz * 16));
-    CR_TRY(ensure(c, c->rbpoff, NEz * 4));
-    CR_TRY(ensure(c, c->rbcmap, (size_t)(ntC + 1) * 4));
-    CR_TRY(ensure(c, c->tilehist, ntile_b * 4));
-    CR_TRY(ensure(c, c->tilebase, ntile_b * 4));
-    CR_TRY(ensure(c, c->pva, Pz * 4));
-    CR_TRY(ensure(c, c->hist, (size_t)(4 * 256 + 16) * 4));
-    const size_t lbytes = std::max<size_t>((size_t)ntB * ndB, (size_t)ntC * ndC) * 8;
-    if (lbytes > c->look.bytes || !c->look.p) {
-      CR_TRY(ensure(c, c->look, lbytes));
-      CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, str));
-      c->epoch = 0;
-    }
-    pA = P_<uint32_t>(c->pva);
-    uint32_t* ctr = P_<uint32_t>(c->hist) + 4 * 256 + 8;  // tile tickets of k_rowbin / k_colsort
-    CR_CUDA(c, cudaMemsetAsync(ctr, 0, 8, str));
-    CR_CUDA(c, cudaMemsetAsync(c->tilehist.p, 0, ntile_b * 4, str));
-    unsigned long long* lk = P_<unsigned long long>(c->look);
-    uint32_t* rowtab = P_<uint32_t>(c->rowhist) + 2 * kRbMaxRows;  // [3][kRowTab]
-    if (ndC == 512) k_row_tables<512><<<1, kRbThreads, 0, str>>>(rowhist, rowtab);
-    else k_row_tables<256><<<1, kRbThreads, 0, str>>>(rowhist, rowtab);
-    CR_LAUNCHED(c);
-    if (NE > 0) {
-      if (++c->epoch >= (1u << 30)) {
-        CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, str));
-        c->epoch = 1;
-      }
-#define CR_ROWBIN(ND)                                                                         \
-  cudaFuncSetAttribute(k_rowbin<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRbDynSmem); \
-  k_rowbin<ND><<<ntB, kRbThreads, kRbDynSmem, str>>>(rec_sorted, P_<uint4>(c->slots),                 \
-                                            P_<uint32_t>(c->offs), nvis, NE,                 \
-                                            P_<uint32_t>(c->tfirst), P_<uint4>(c->bigent),   \
-                                            rowtab, P_<uint4>(c->rbent), lk, ctr, c->epoch)
-      if (ndB == 512) { CR_ROWBIN(512); } else { CR_ROWBIN(256); }
-#undef CR_ROWBIN
-      CR_LAUNCHED(c);
-    }
-    CR_TRACE(c, "row entries");
-    CR_CUDA(c, cudaEventRecord(c->ev[3], str));
-    if (NE > 0) {
-      const long long nbs = (NE + kScanTile - 1) / kScanTile;
-      uint32_t* ticket = nullptr;
-      unsigned long long* slk = nullptr;
-      CR_TRY(scan_lookback(c, nbs, &ticket, &slk));
-#define CR_ROWSCAN(ND)                                                                        \
-  k_rowscan<ND><<<(unsigned)nbs, kScanThreads, 0, str>>>(                                   \
-      P_<uint4>(c->rbent), NE, rowtab, P_<uint32_t>(c->rbpoff), P_<uint32_t>(c->tilehist),   \
-      P_<uint32_t>(c->rbcmap), slk, ticket, c->sepoch)
-      if (ndC == 512) CR_ROWSCAN(512); else CR_ROWSCAN(256);
-#undef CR_ROWSCAN
-      CR_LAUNCHED(c);
-    }
-    if (ndC == 512)
-      k_tile_bases<512><<<nbr, 512, 0, str>>>(rowhist, P_<uint32_t>(c->tilehist), P_<uint32_t>(c->tilebase));
-    else
-      k_tile_bases<256><<<nbr, 512, 0, str>>>(rowhist, P_<uint32_t>(c->tilehist), P_<uint32_t>(c->tilebase));
-    CR_LAUNCHED(c);
-    if (P > 0) {
-      if (++c->epoch >= (1u << 30)) {
-        CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, str));
-        c->epoch = 1;
-      }
-#define CR_COLSORT(ND)                                                                        \
-  cudaFuncSetAttribute(k_colsort<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCsDynSmem); \
-  k_colsort<ND><<<(unsigned)ntC, kRbThreads, kCsDynSmem, str>>>(                                     \
-      P_<uint4>(c->rbent), P_<uint32_t>(c->rbpoff), NE, rowtab, P_<uint32_t>(c->rbcmap),     \
-      P_<uint32_t>(c->tilebase), pA, lk, ctr + 1, c->epoch)
-      if (ndC == 512) { CR_COLSORT(512); } else { CR_COLSORT(256); }
-#undef CR_COLSORT
-      CR_LAUNCHED(c);
-    }
-    const size_t nSE = (size_t)TX * TY * K;
-    CR_TRY(ensure(c, c->S, nSE * 4));
-    CR_TRY(ensure(c, c->E, nSE * 4));
-    CR_CUDA(c, cudaMemsetAsync(c->S.p, 0, nSE * 4, str));
-    CR_CUDA(c, cudaMemsetAsync(c->E.p, 0, nSE * 4, str));
-    k_ranges_rb<<<grid_for((long long)ntile_b * K, 256), 256, 0, str>>>(
-        pA, P_<uint32_t>(c->tilebase), P_<uint32_t>(c->tilehist), P_<uint32_t>(c->S),
-        P_<uint32_t>(c->E));
-    CR_LAUNCHED(c);
-  } else {
-  if (nvis > 0) {
-    CR_TRY(launch_counts());
     CR_LAUNCHED(c);
     CR_TRACE(c, "count");
     CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->cnt)}, Scan::OutStore{P_<uint32_t>(c->offs)},
@@ -1110,8 +907,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->pva, Pz * 4));
   CR_TRY(ensure(c, c->ptb, Pz * 4));
   CR_TRY(ensure(c, c->pvb, Pz * 4));
-  tA = P_<uint32_t>(c->pta);
-  pA = P_<uint32_t>(c->pva);
+  uint32_t *tA = P_<uint32_t>(c->pta), *pA = P_<uint32_t>(c->pva);
   uint32_t *tB = P_<uint32_t>(c->ptb), *pB = P_<uint32_t>(c->pvb);
   if (P > 0) {
     // big-footprint records are emitted on a forked stream, concurrently with
@@ -1175,7 +971,6 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
         tA, P, P_<uint32_t>(c->S), P_<uint32_t>(c->E));
     CR_LAUNCHED(c);
   }
-  }  // emission + LSD tail
   CR_TRACE(c, "tile sort+ranges");
   CR_CUDA(c, cudaEventRecord(c->ev[4], str));
 
@@ -1314,16 +1109,8 @@ cr_status cr_get_sorted_pairs(cr_ctx* c, uint64_t* keys, uint32_t* pay, size_t* 
     CR_TRY(ensure(c, kb, (size_t)c->P * 8));
     cr_status s = ensure(c, pb, (size_t)c->P * 4);
     if (s != CR_OK) { release(kb); return s; }
-    const uint32_t* slot = c->final_t;
-    if (c->rb_frame) {  // rebuild the (t, k) slot of every pair from the ranges
-      s = ensure(c, c->slotkeys, (size_t)c->P * 4);
-      if (s != CR_OK) { release(kb); release(pb); return s; }
-      k_fill_slots<<<148 * 16, 256, 0, c->stream>>>(P_<uint32_t>(c->S), P_<uint32_t>(c->E),
-                                                  P_<uint32_t>(c->slotkeys));
-      slot = P_<uint32_t>(c->slotkeys);
-    }
     k_make_keys<<<grid_for(c->P, 256), 256, 0, c->stream>>>(
-        slot, c->final_v, P_<uint32_t>(c->dkey), c->P, P_<unsigned long long>(kb),
+        c->final_t, c->final_v, P_<uint32_t>(c->dkey), c->P, P_<unsigned long long>(kb),
         P_<uint32_t>(pb));
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e == cudaSuccess) e = cudaMemcpy(keys, kb.p, (size_t)c->P * 8, cudaMemcpyDeviceToHost);

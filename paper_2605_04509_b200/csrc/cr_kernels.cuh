@@ -590,12 +590,7 @@ constexpr int kBinWarps = kBinThreads / 32;
 // records per step, halving the per-record share of loads, group reductions,
 // the item prefix scan and the slot write (measured: binning 7.56 -> 6.58 ms
 // at config C; VPL = 4: 6.54 ms, not worth its 77 registers).
-// RB (row-bucketed binning tail, cr_rowbin.cuh): cnt[g] = the record's union
-// ROW count (its row entries) instead of its pair count, and the band's
-// per-row entry / pair totals are accumulated into rowhist[0][row - row0] /
-// rowhist[1][row - row0] (shared-memory histogram per CTA, flushed once).
-constexpr int kRbMaxRows = 512;  // band tile rows / tile columns of the RB path
-template <int G, int VPL, bool RB = false>
+template <int G, int VPL>
 __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restrict__ recs,
                                                         uint32_t n,
                                                         const float4* __restrict__ mean4,
@@ -603,12 +598,8 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
                                                         uint32_t* __restrict__ cnt,
                                                         uint4* __restrict__ slots,
                                                         uint32_t* __restrict__ big,
-                                                        uint32_t* __restrict__ n_big,
-                                                        uint32_t* __restrict__ rowhist = nullptr) {
+                                                        uint32_t* __restrict__ n_big) {
   extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic)
-  __shared__ uint32_t s_rh[RB ? 2 * kRbMaxRows : 1];
-  if (RB)
-    for (int q = threadIdx.x; q < 2 * kRbMaxRows; q += blockDim.x) s_rh[q] = 0u;
   __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
   __shared__ int s_flag[kBinWarps][32];
   __shared__ int s_src[kBinWarps][32];
@@ -751,14 +742,7 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
       const bool wr = active && fast && !slow;
       uint32_t pc = 0;
       if (wr)
-        for (int t = v; t < kSlotRows; t += G) {
-          const uint32_t pt = (uint32_t)__popcll(s_mask[w][gi][t]);
-          pc += pt;
-          if (RB && t < nrows) {
-            atomicAdd(&s_rh[rmin - c_fp.row0 + t], 1u);
-            if (pt) atomicAdd(&s_rh[kRbMaxRows + rmin - c_fp.row0 + t], pt);
-          }
-        }
+        for (int t = v; t < kSlotRows; t += G) pc += (uint32_t)__popcll(s_mask[w][gi][t]);
 #pragma unroll
       for (int q = 1; q < G; q <<= 1) pc += __shfl_xor_sync(0xffffffffu, pc, q);
       if (wr) c = pc;
@@ -776,16 +760,8 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
       slots[4ull * o] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
       big[atomicAdd(n_big, 1u)] = (uint32_t)o;
     }
-    if (active && lead) cnt[o] = RB ? ((active && fast && !slow) ? (uint32_t)nrows : 0u) : c;
+    if (active && lead) cnt[o] = c;
     __syncwarp();
-  }
-  if (RB) {
-    __syncthreads();
-    const int nb = c_fp.row1 - c_fp.row0;
-    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
-      if (s_rh[q]) atomicAdd(&rowhist[q], s_rh[q]);
-      if (s_rh[kRbMaxRows + q]) atomicAdd(&rowhist[kRbMaxRows + q], s_rh[kRbMaxRows + q]);
-    }
   }
 }
 

@@ -103,3 +103,14 @@ def cfgA_pair_local():
     g.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset)
     g.set_camera_rig(c.make_rig())
     return g, c
+
+
+def test_wide_panel_8320px():
+    # 8320 px wide (520 tile columns over 3 tile rows: the tile sort's high
+    # digit spans few values and its histogram is aggregated), vs the oracle
+    _need_gpu()
+    W, H, N = 8320, 48, 6
+    sc = sy.random_scene(3000, 0, seed=47, scale_median=0.02)
+    cams = sy.orbit_rig(N, 6.0, W, H, radius=3.0, height=0.2, fov_y_deg=20.0)
+    g, o = make_pair(sc, W, H, N, 13.1, 0.17, 1.3, cams)
+    check_frame(g, o, 3)
