@@ -159,6 +159,13 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  *                  CR_FLAG_VIEW_FRAMES (implies the full-frame render) returns
  *                  those per-view frames instead of interlacing them: out is
  *                  [N][rows][W][3], out_bytes >= N times the band size.
+ *   view_batch     full-frame render only: views per pass (the paper's
+ *                  "3DGS (batch=B)" baseline, T2 P:520; 1 = plain
+ *                  per-view 3DGS): the N views are rendered B at a time, each
+ *                  pass running preprocess, binning, sort and the full-frame
+ *                  composite for its views only, then the frames are
+ *                  interlaced once.  Must be a multiple of cluster_size;
+ *                  0 (or >= N) = all N views in one pass.  Ignored otherwise.
  * out: caller-owned, [rows][W][3] of the band (rows = clipped band height),
  * out_bytes must be >= rows*W*3*(1 or 4).  out_on_device selects a device
  * pointer (written on the stream) or a host pointer (copied back, the call
@@ -177,6 +184,7 @@ typedef struct {
   int32_t tile_row_begin, tile_row_end;
   int32_t flags;         /* bit 0: count blend evaluations into cr_stats.evals
                             (instrumented composite; slower, for rooflines)   */
+  int32_t view_batch;    /* full-frame baseline: views per pass (0 = all)    */
 } cr_render_opts;
 
 typedef struct {

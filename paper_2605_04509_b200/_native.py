@@ -47,7 +47,7 @@ class RenderOpts(C.Structure):
     _fields_ = [("cluster_size", C.c_int32), ("remap", C.c_int32), ("kernel", C.c_int32),
                 ("background", C.c_float * 3), ("output_format", C.c_int32),
                 ("tile_row_begin", C.c_int32), ("tile_row_end", C.c_int32),
-                ("flags", C.c_int32)]
+                ("flags", C.c_int32), ("view_batch", C.c_int32)]
 
 
 class Stats(C.Structure):

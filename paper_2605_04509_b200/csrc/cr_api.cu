@@ -136,6 +136,7 @@ struct cr_ctx {
   cudaEvent_t ev[6] = {};
   cudaStream_t side = nullptr;     // forked stream for concurrent big-record emission
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_batch[2] = {};    // around a batched full-frame render
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
   int exp = 0;         // CR_EXP (read once at cr_create): developer A/B switches, 0 = shipped path
@@ -424,6 +425,7 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
     return CR_ERR_CUDA;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  for (auto& e : c->ev_batch) cudaEventCreate(&e);
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
@@ -446,6 +448,8 @@ void cr_destroy(cr_ctx* c) {
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
   for (DevBuf* b : all) release(*b);
   for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_batch)
     if (e) cudaEventDestroy(e);
   if (c->side) {
     cudaStreamSynchronize(c->side);
@@ -619,6 +623,96 @@ cr_status cr_make_orbit_rig(const cr_display* d, const float look_at[3], const f
   return CR_OK;
 }
 
+// The full-frame baseline B views per pass (the paper's "3DGS (batch=B)",
+// P:520): each pass renders views [v0, v0 + B) as a B-view frame with
+// CR_FLAG_VIEW_FRAMES straight into its slice of the [N][rows][W][3] frame
+// buffer (its own preprocess, binning, sort and full-frame composite), then
+// the N frames are interlaced by V once.
+static cr_status render_view_batches(cr_ctx* c, const cr_render_opts* o, void* out,
+                                     size_t out_bytes, int out_on_device, cr_stats* st) {
+  const int N = c->disp.num_views, W = c->disp.width, H = c->disp.height;
+  const int B = o->view_batch;
+  if (B % o->cluster_size != 0)
+    return fail(c, CR_ERR_INVALID_ARG, "view_batch %d is not a multiple of cluster_size %d", B,
+                o->cluster_size);
+  int row0 = o->tile_row_begin, row1 = o->tile_row_end;
+  if (row0 == 0 && row1 == 0) row1 = c->TY;
+  if (row0 < 0 || row1 > c->TY || row0 >= row1)
+    return fail(c, CR_ERR_INVALID_ARG, "tile rows [%d,%d) outside [0,%d)", row0, row1, c->TY);
+  const int rows_px = std::min(H, row1 * 16) - row0 * 16;
+  const bool view_frames = (o->flags & CR_FLAG_VIEW_FRAMES) != 0;
+  const size_t plane = (size_t)rows_px * W * 3 * (o->output_format ? 4 : 1);
+  const size_t obytes = view_frames ? (size_t)N * plane : plane;
+  if (out_bytes < obytes) return fail(c, CR_ERR_INVALID_ARG, "out_bytes %zu < %zu", out_bytes, obytes);
+  cudaSetDevice(c->device);
+  void* fr = out;
+  if (!(view_frames && out_on_device)) {
+    CR_TRY(ensure(c, c->frames, (size_t)N * plane));
+    fr = c->frames.p;
+  }
+  CR_CUDA(c, cudaEventRecord(c->ev_batch[0], c->stream));
+  const std::vector<CamDev> cams = c->cams;
+  const std::vector<CamConstDev> ccon = c->ccon;
+  cr_render_opts oi = *o;
+  oi.flags = (o->flags & CR_FLAG_COUNT_EVALS) | CR_FLAG_VIEW_FRAMES;
+  oi.view_batch = 0;
+  cr_stats acc{};
+  int launches = 0;
+  cr_status r = CR_OK;
+  for (int v0 = 0; v0 < N && r == CR_OK; v0 += B) {
+    const int nb = std::min(B, N - v0);
+    c->cams.assign(cams.begin() + v0, cams.begin() + v0 + nb);
+    c->ccon.assign(ccon.begin() + v0, ccon.begin() + v0 + nb);
+    c->disp.num_views = nb;
+    cr_stats sb{};
+    r = cr_render_interlaced(c, &oi, (char*)fr + (size_t)v0 * plane, (size_t)nb * plane, 1,
+                             st ? &sb : nullptr);
+    launches += c->launches;
+    acc.pairs += sb.pairs;
+    acc.visible_ik += sb.visible_ik;
+    acc.culled_near += sb.culled_near;
+    acc.culled_degenerate += sb.culled_degenerate;
+    acc.culled_opacity += sb.culled_opacity;
+    acc.evals += sb.evals;
+    acc.num_clusters += sb.num_clusters;
+    acc.emit_fallback += sb.emit_fallback;
+  }
+  c->cams = cams;
+  c->ccon = ccon;
+  c->disp.num_views = N;
+  if (r != CR_OK) return r;
+  c->has_frame = false;  // introspection would describe the last pass only
+  cudaStream_t str = c->stream;
+  if (!view_frames) {
+    void* dst = out;
+    if (!out_on_device) {
+      CR_TRY(ensure(c, c->stage_out, plane));
+      dst = c->stage_out.p;
+    }
+    const long long nsub = (long long)rows_px * W * 3;
+    const unsigned gi = (unsigned)std::min<long long>(grid_for(nsub, 256), 148 * 32);
+    if (o->output_format == 0) k_interlace<0><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), fr, dst, rows_px);
+    else k_interlace<1><<<gi, 256, 0, str>>>(P_<uint8_t>(c->V), fr, dst, rows_px);
+    c->launches = launches;
+    CR_LAUNCHED(c);
+    launches = c->launches;
+    if (!out_on_device) CR_CUDA(c, cudaMemcpyAsync(out, dst, plane, cudaMemcpyDeviceToHost, str));
+  } else if (!out_on_device) {
+    CR_CUDA(c, cudaMemcpyAsync(out, fr, (size_t)N * plane, cudaMemcpyDeviceToHost, str));
+  }
+  CR_CUDA(c, cudaEventRecord(c->ev_batch[1], str));
+  c->launches = launches;
+  if (!out_on_device || st) CR_CUDA(c, cudaStreamSynchronize(str));
+  if (st) {
+    *st = acc;
+    st->bit_k = 0;
+    st->launches = launches;
+    cudaEventElapsedTime(&st->ms_total, c->ev_batch[0], c->ev_batch[1]);
+    st->device_bytes = c->device_bytes;
+  }
+  return CR_OK;
+}
+
 cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, size_t out_bytes,
                                int out_on_device, cr_stats* st) {
   if (!c || !o || !out) return CR_ERR_INVALID_ARG;
@@ -635,6 +729,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (o->output_format != 0 && o->output_format != 1) return fail(c, CR_ERR_INVALID_ARG, "format");
   const bool view_frames = (o->flags & CR_FLAG_VIEW_FRAMES) != 0;
   const bool fullframe = view_frames || (o->flags & CR_FLAG_FULLFRAME) != 0;
+  if (o->view_batch < 0) return fail(c, CR_ERR_INVALID_ARG, "view_batch %d < 0", o->view_batch);
+  if (fullframe && o->view_batch > 0 && o->view_batch < N)
+    return render_view_batches(c, o, out, out_bytes, out_on_device, st);
   for (int u = 0; u < 3; ++u)
     if (!std::isfinite(o->background[u])) return fail(c, CR_ERR_NONFINITE, "background");
   int row0 = o->tile_row_begin, row1 = o->tile_row_end;
@@ -677,7 +774,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_rep, rep.data(), sizeof(int) * K, 0,
                                      cudaMemcpyHostToDevice, str));
   {  // cluster motion bounds for the band / frame pre-cull (fp64, rounded up)
-    std::vector<float4> clb(K);
+    std::vector<float4> clb(K), clax(K), clbx(K);
     std::vector<float> cldb(K);
     double maxdA = 0.0;
     for (int k = 0; k < K; ++k) {
@@ -725,6 +822,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
           if (!std::isfinite(cc[a])) cc[a] = 0.0;
         }
       double dA = 0.0, db = 0.0;  // the bound holds for ANY c; the centre only tightens it
+      double dAa[3] = {0, 0, 0}, dba[3] = {0, 0, 0};  // per camera-space axis
       for (const auto& q : mv) {
         double fro = 0.0, b2 = 0.0;
         for (int a = 0; a < 9; ++a) fro += q[a] * q[a];
@@ -732,6 +830,10 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
           double v = q[9 + a];
           for (int z = 0; z < 3; ++z) v += q[a * 3 + z] * cc[z];
           b2 += v * v;
+          const double rn = std::sqrt(q[a * 3] * q[a * 3] + q[a * 3 + 1] * q[a * 3 + 1] +
+                                      q[a * 3 + 2] * q[a * 3 + 2]);
+          dAa[a] = std::max(dAa[a], rn);
+          dba[a] = std::max(dba[a], std::fabs(v));
         }
         dA = std::max(dA, std::sqrt(fro));
         db = std::max(db, std::sqrt(b2));
@@ -739,10 +841,18 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       clb[k] = make_float4((float)cc[0], (float)cc[1], (float)cc[2], (float)(dA * 1.0001 + 1e-7));
       maxdA = std::max(maxdA, dA);
       cldb[k] = (float)(db * 1.0001 + 1e-6);
+      clax[k] = make_float4((float)(dAa[0] * 1.0001 + 1e-7), (float)(dAa[1] * 1.0001 + 1e-7),
+                            (float)(dAa[2] * 1.0001 + 1e-7), 0.f);
+      clbx[k] = make_float4((float)(dba[0] * 1.0001 + 1e-6), (float)(dba[1] * 1.0001 + 1e-6),
+                            (float)(dba[2] * 1.0001 + 1e-6), 0.f);
     }
     CR_CUDA(c, cudaMemcpyToSymbolAsync(c_clb, clb.data(), sizeof(float4) * K, 0,
                                        cudaMemcpyHostToDevice, str));
     CR_CUDA(c, cudaMemcpyToSymbolAsync(c_cldb, cldb.data(), sizeof(float) * K, 0,
+                                       cudaMemcpyHostToDevice, str));
+    CR_CUDA(c, cudaMemcpyToSymbolAsync(c_clax, clax.data(), sizeof(float4) * K, 0,
+                                       cudaMemcpyHostToDevice, str));
+    CR_CUDA(c, cudaMemcpyToSymbolAsync(c_clbx, clbx.data(), sizeof(float4) * K, 0,
                                        cudaMemcpyHostToDevice, str));
     c->motion_bound = maxdA < (double)kMotionBoundMax;  // narrow clusters: one projection
   }
@@ -803,9 +913,10 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (M > 0) {
     const unsigned g = grid_for(M, 128);
 #define CR_PRE(D)                                                                               \
-  if (c->motion_bound) CR_PRE2(D, true); else CR_PRE2(D, false)
-#define CR_PRE2(D, MBV)                                                                         \
-  k_preprocess<D, MBV><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
+  if (c->motion_bound) { if (c->exp & 64) CR_PRE2(D, true, 6); else if (c->exp & 128) CR_PRE2(D, true, 5); else CR_PRE2(D, true, 1); } \
+  else { if (c->exp & 64) CR_PRE2(D, false, 6); else if (c->exp & 128) CR_PRE2(D, false, 5); else CR_PRE2(D, false, 1); }
+#define CR_PRE2(D, MBV, MB)                                                                     \
+  k_preprocess<D, MBV, MB><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
                                       P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
                                       P_<float4>(c->rec0) + 1, P_<float4>(c->geom),                 \
                                       P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters, sc + 16)
@@ -984,11 +1095,16 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   const float4* m4 = P_<float4>(c->mean4);
   const bool count = (o->flags & CR_FLAG_COUNT_EVALS) != 0;
   unsigned long long* evals = counters + 3;
+  // grids under ~3 waves of 148 x 10 resident CTAs (narrow row bands): split
+  // each tile's chunks over up to 4 CTAs (measured: see DESIGN.md §7)
+  // (CR_EXP bit 5: never split, so tests cover both store paths on small frames)
+  const int tsplit = (c->exp & 32) ? 1 : (int)std::min<long long>(
+      4, std::max<long long>(1, (3LL * 148 * CR_COMP_MINB + ntile - 1) / std::max(1u, ntile)));
 #define CR_STAGED1(F, CNT, VAR)                                                                \
-  k_composite_staged<F, CNT, kCompWarps, VAR><<<ntile, kCompWarps * 32, 0, str>>>(           \
+  k_composite_staged<F, CNT, kCompWarps, VAR><<<ntile * tsplit, kCompWarps * 32, 0, str>>>(  \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
-      P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals)
+      P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals, tsplit)
 #define CR_STAGED(F, CNT) CR_STAGED1(F, CNT, 0)
 #define CR_THREAD(F, CNT)                                                                     \
   k_composite_thread<F, CNT><<<ntile, kTileSub, 0, str>>>(                                    \

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
     const uint32_t* __restrict__ S, const uint32_t* __restrict__ E,
     const uint32_t* __restrict__ vals, const float4* __restrict__ rec0,
     const float4* __restrict__ rec1, const float4* __restrict__ mean4, void* __restrict__ out,
-    unsigned long long* __restrict__ evals) {
+    unsigned long long* __restrict__ evals, int tsplit) {
   __shared__ float4 s_rec[NW][32];  // v1: register pipeline
   __shared__ float4 s_col[NW][32];
   __shared__ float2 s_mu[NW][kSlots][32];
@@ -199,7 +199,11 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
   __shared__ int s_next;
   const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
   const long long M = c_fp.M;
-  const int t = c_fp.row0 * TX + blockIdx.x;
+  // tsplit > 1 (grids under ~3 waves, e.g. narrow row bands): tsplit CTAs share
+  // one tile, CTA `part` taking chunks part, part + tsplit, ... and storing its
+  // subpixels directly, so the densest tiles no longer set the band's time
+  const int t = c_fp.row0 * TX + (int)(blockIdx.x / (unsigned)tsplit);
+  const int part = (int)(blockIdx.x % (unsigned)tsplit);
   const int tx = t % TX, ty = t / TX;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ uint32_t s_ch[kMaxChunks];
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
   unsigned long long nev = 0;
   for (;;) {
     int c = 0;
-    if (lane == 0) c = atomicAdd(&s_next, 1);
+    if (lane == 0) c = atomicAdd(&s_next, 1) * tsplit + part;
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= nch) break;
     const uint32_t ch = ch_t[c];
@@ -334,12 +338,23 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
         cur = nxt;
       }
       __syncwarp();
-      if (active) s_out[l] = C + c_fp.bg[u] * T;
+      if (active) {
+        const float v = C + c_fp.bg[u] * T;
+        if (tsplit == 1) {
+          s_out[l] = v;
+        } else {
+          const long long o = ((long long)(y - c_fp.row0 * 16) * W + x) * 3 + u;
+          if (FMT == 0) ((uint8_t*)out)[o] = (uint8_t)quant_u8(v);
+          else ((float*)out)[o] = v;
+        }
+      }
     }
   }
   if (COUNT) add_evals(evals, nev);
-  __syncthreads();
-  store_tile<FMT>(s_out, out, tx, ty, W, H, c_fp.row0 * 16);
+  if (tsplit == 1) {
+    __syncthreads();
+    store_tile<FMT>(s_out, out, tx, ty, W, H, c_fp.row0 * 16);
+  }
 }
 
 // ===========================================================================

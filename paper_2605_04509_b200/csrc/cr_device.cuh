@@ -69,6 +69,11 @@ __constant__ int c_rep[kMaxViews];
 // db = max_j |(A_j - I) c + b_j|.  c_clb[k] = (c.x, c.y, c.z, dA), c_cldb[k] = db.
 __constant__ float4 c_clb[kMaxViews];
 __constant__ float c_cldb[kMaxViews];
+// Per camera-space axis a: |p_j,a - p_a| <= dA_a |p - c| + db_a with dA_a = max_j
+// ||row a of (A_j - I)||, db_a = max_j |((A_j - I) c + b_j)_a| (a row band only
+// needs the y shift, which a horizontal camera motion keeps small).
+__constant__ float4 c_clax[kMaxViews];  // (dA_x, dA_y, dA_z, 0)
+__constant__ float4 c_clbx[kMaxViews];  // (db_x, db_y, db_z, 0)
 __constant__ FrameParams c_fp;
 
 // ---------------------------------------------------------------- exact ops

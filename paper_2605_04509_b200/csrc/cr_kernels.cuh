@@ -424,8 +424,8 @@ __device__ __forceinline__ bool may_touch_band_views(int k, float mx, float my, 
 // camera-space point p: every view j of cluster k sees p_j = A_j p + b_j, and
 // |p_j - p| <= D = dA |p - c| + db (c_clb: rigid-motion bound of the cluster
 // about its least-squares fixed point c, fp64 on the host, rounded up), so
-// view j's image x lies within fx D (1 + |p.x/p.z|) / (p.z - D) of the rep's
-// (same for y).  When even the box grown by that shift (and by pads for fp32
+// view j's image x lies within fx (D_x + |p.x/p.z| D_z) / (p.z - D_z) of the
+// rep's (same for y), with per-axis bounds D_a (c_clax / c_clbx).  When even the box grown by that shift (and by pads for fp32
 // rounding: 1 %, 2e-5 relative, 3 px) misses the band rows x frame columns, no
 // view can give the record a tile there: the exact union (O8) is empty and
 // skipping the record changes no result.  Near-znear depths return true.
@@ -439,23 +439,28 @@ __device__ __forceinline__ bool may_touch_band(int k, int jr, const F3& p, float
   const float ylo = 16.0f * (float)c_fp.row0 - 16.0f, yhi = 16.0f * (float)c_fp.row1 + 16.0f;
   const float xlo = -16.0f, xhi = 16.0f * (float)c_fp.TX + 16.0f;
   const CamDev& c = c_cams[jr];
-  const float4 cl = c_clb[k];
+  const float4 cl = c_clb[k], ax = c_clax[k], bx = c_clbx[k];
   const float dx = p.x - cl.x, dy = p.y - cl.y, dz = p.z - cl.z;
-  const float D = (cl.w * sqrtf(dx * dx + dy * dy + dz * dz) + c_cldb[k]) * 1.001f +
-                  1e-5f * (fabsf(p.x) + fabsf(p.y) + fabsf(p.z));
-  const float zlo = p.z - D;
+  const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+  const float pad = 1e-5f * (fabsf(p.x) + fabsf(p.y) + fabsf(p.z));
+  // per-axis displacement bounds (each also <= the isotropic one)
+  const float Dx = (ax.x * dist + bx.x) * 1.001f + pad;
+  const float Dy = (ax.y * dist + bx.y) * 1.001f + pad;
+  const float Dz = (ax.z * dist + bx.z) * 1.001f + pad;
+  const float zlo = p.z - Dz;
   if (zlo < 2.0f * c_fp.znear) return true;  // too close to call
   const float iz = 1.0f / p.z, izl = 1.0f / zlo;
   const float u = p.x * iz, v = p.y * iz;
   const float ex = c.fx * u + c.cx, ey = c.fy * v + c.cy;
-  const float sx = c.fx * D * (1.0f + fabsf(u)) * izl * 1.01f + 2e-5f * fabsf(ex) + 3.0f;
-  const float sy = c.fy * D * (1.0f + fabsf(v)) * izl * 1.01f + 2e-5f * fabsf(ey) + 3.0f;
+  // x_j - x = fx (e_x - u e_z) / (p.z + e_z), |e_a| <= D_a (same for y)
+  const float sx = c.fx * (Dx + fabsf(u) * Dz) * izl * 1.01f + 2e-5f * fabsf(ex) + 3.0f;
+  const float sy = c.fy * (Dy + fabsf(v) * Dz) * izl * 1.01f + 2e-5f * fabsf(ey) + 3.0f;
   return ey + eyw + sy >= ylo && ey - eyw - sy <= yhi && ex + exw + sx >= xlo &&
          ex - exw - sx <= xhi;
 }
 
-template <int DEG, bool MB>
-__global__ void __launch_bounds__(128) k_preprocess(
+template <int DEG, bool MB, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
     const float* __restrict__ shsoa, float4* __restrict__ rec0, float4* __restrict__ rec1,
     float4* __restrict__ geom, uint32_t* __restrict__ dkey, uint32_t* __restrict__ vis,

@@ -114,3 +114,34 @@ def test_wide_panel_8320px():
     cams = sy.orbit_rig(N, 6.0, W, H, radius=3.0, height=0.2, fov_y_deg=20.0)
     g, o = make_pair(sc, W, H, N, 13.1, 0.17, 1.3, cams)
     check_frame(g, o, 3)
+
+
+@pytest.mark.parametrize("W,H", [(256, 144), (250, 138)])
+def test_tile_split_equals_whole_tile_composite(W, H):
+    # small grids split each tile's chunks over several CTAs that store their
+    # subpixels directly; CR_EXP bit 5 forces one CTA per tile (shared-memory
+    # tile + 16-byte row stores, scalar at the ragged edge): identical frames
+    _need_gpu()
+    import os
+    from paper_2605_04509_b200 import CoherentRaster
+    sc = sy.random_scene(4000, 1, seed=49, scale_median=0.04)
+    cams = sy.orbit_rig(8, 8.0, W, H, radius=3.0, height=0.2, fov_y_deg=50.0)
+    imgs = []
+    for exp in ("0", "32"):
+        old = os.environ.get("CR_EXP")
+        os.environ["CR_EXP"] = exp
+        try:
+            g = CoherentRaster(0)
+        finally:
+            if old is None:
+                del os.environ["CR_EXP"]
+            else:
+                os.environ["CR_EXP"] = old
+        g.upload_gaussians(sc)
+        g.set_display(W, H, 8, 12.5, 0.25, 1.5)
+        g.set_camera_rig(cams)
+        for fmt in ("float", "rgb8"):
+            imgs.append(g.render(cluster_size=4, output_format=fmt).cpu().numpy())
+            imgs.append(g.render(cluster_size=4, output_format=fmt, rows=(2, 6)).cpu().numpy())
+    for a, b in zip(imgs[:4], imgs[4:]):
+        assert np.array_equal(a, b)

@@ -362,6 +362,29 @@ def test_fullframe_baseline_equals_subpixel_s1(cfgA_pair):
                           g.render(4, output_format="float").cpu().numpy())
 
 
+def test_fullframe_view_batches(cfgA_pair):
+    # the paper's batched full-frame 3DGS baseline ("3DGS (batch=B)", P:520;
+    # B=1 plain 3DGS): views rendered B per pass (own preprocess, binning and
+    # sort per pass) then interlaced once == all views in one pass, bit for bit
+    g, o = cfgA_pair
+    for s in (1, 2):
+        ref = g.render(s, output_format="float", fullframe=True).cpu().numpy()
+        ref_v = g.render(s, output_format="rgb8", view_frames=True, rows=(1, 5)).cpu().numpy()
+        for vb in (1, 3, 4, 6):
+            if vb % s:
+                continue
+            got = g.render(s, output_format="float", fullframe=True, view_batch=vb, stats=True)
+            assert np.array_equal(got.cpu().numpy(), ref)
+            got_v = g.render(s, output_format="rgb8", view_frames=True, rows=(1, 5), view_batch=vb)
+            assert np.array_equal(got_v.cpu().numpy(), ref_v)
+    host = np.zeros(g.band_shape(None), np.uint8)
+    g.render(1, output_format="rgb8", fullframe=True, view_batch=3, out=host)
+    assert np.array_equal(host, g.render(1, output_format="rgb8", fullframe=True).cpu().numpy())
+    from paper_2605_04509_b200._native import CrError
+    with pytest.raises(CrError):
+        g.render(2, fullframe=True, view_batch=3)  # not a multiple of the cluster size
+
+
 @pytest.mark.parametrize("s", [16, 18, 3])
 def test_large_and_odd_clusters(s):
     """Cluster sizes beyond 8: G = 16 (P2K's s=16) and G = 32 (P4K's s=18)
