@@ -913,10 +913,9 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   if (M > 0) {
     const unsigned g = grid_for(M, 128);
 #define CR_PRE(D)                                                                               \
-  if (c->motion_bound) { if (c->exp & 64) CR_PRE2(D, true, 6); else if (c->exp & 128) CR_PRE2(D, true, 5); else CR_PRE2(D, true, 1); } \
-  else { if (c->exp & 64) CR_PRE2(D, false, 6); else if (c->exp & 128) CR_PRE2(D, false, 5); else CR_PRE2(D, false, 1); }
-#define CR_PRE2(D, MBV, MB)                                                                     \
-  k_preprocess<D, MBV, MB><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
+  if (c->motion_bound) CR_PRE2(D, true); else CR_PRE2(D, false)
+#define CR_PRE2(D, MBV)                                                                         \
+  k_preprocess<D, MBV><<<g, 128, 0, str>>>(P_<float4>(c->mean4), P_<float4>(c->cov8),               \
                                       P_<float>(c->shsoa), P_<float4>(c->rec0),                 \
                                       P_<float4>(c->rec0) + 1, P_<float4>(c->geom),                 \
                                       P_<uint32_t>(c->dkey), P_<uint32_t>(c->vis), counters, sc + 16)

@@ -459,8 +459,10 @@ __device__ __forceinline__ bool may_touch_band(int k, int jr, const F3& p, float
          ex - exw - sx <= xhi;
 }
 
-template <int DEG, bool MB, int MINB = 1>
-__global__ void __launch_bounds__(128, MINB) k_preprocess(
+// 116 registers, 4 CTAs/SM (measured at config C: capping at 96 / 80
+// registers for 5 / 6 CTAs/SM gives 1.14 / 1.38 ms against 1.13 ms)
+template <int DEG, bool MB>
+__global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
     const float* __restrict__ shsoa, float4* __restrict__ rec0, float4* __restrict__ rec1,
     float4* __restrict__ geom, uint32_t* __restrict__ dkey, uint32_t* __restrict__ vis,
