@@ -1032,9 +1032,11 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       constexpr int kWB = 256;
       const unsigned eg = (unsigned)std::min<long long>((nvis + 255) / 256, 148 * 16);
       const int sm = 8 * 2 * kWB * 4;
-      cudaFuncSetAttribute(k_emit_rows<kWB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      k_emit_rows<kWB><<<eg, 256, sm, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis, P,
-                                             P_<uint4>(c->slots), tA, pA);
+      // software-pipelined block inputs (measured at config C: binning 6.09 ->
+      // 5.94 ms; P4K unchanged)
+      cudaFuncSetAttribute(k_emit_rows<kWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      k_emit_rows<kWB, true><<<eg, 256, sm, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis, P,
+                                                   P_<uint4>(c->slots), tA, pA);
     };
     auto launch_big = [&]() {
 #define CR_EMITB(GG)                                                                        \

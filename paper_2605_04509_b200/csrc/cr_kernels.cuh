@@ -787,7 +787,43 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
 // less at config C; a run table + max-scan and a pair-flat binary-search
 // decode were both slower.)
 // ===========================================================================
-template <int WB>
+// Per-block inputs of the emission: the records' output offsets, the slot
+// (header + six row masks) and payload r of lane e = b*32 + lane.
+struct EmitIn {
+  uint32_t o, f1, r;
+  uint4 h, s1, s2, s3;
+};
+__device__ __forceinline__ void emit_load_offs(const uint32_t* __restrict__ offs, uint32_t n,
+                                               uint32_t P, uint32_t nblk, uint32_t b, int lane,
+                                               EmitIn& in) {
+  const uint32_t e = b * 32u + (uint32_t)lane;
+  in.o = (b < nblk && e < n) ? offs[e] : P;
+  in.f1 = (b < nblk && b * 32u + 32u < n) ? offs[b * 32u + 32u] : P;
+}
+__device__ __forceinline__ void emit_load_slots(const uint32_t* __restrict__ rec_sorted,
+                                                const uint4* __restrict__ slots, uint32_t n,
+                                                uint32_t nblk, uint32_t b, int lane, EmitIn& in) {
+  const uint32_t e = b * 32u + (uint32_t)lane;
+  uint32_t o1 = __shfl_down_sync(0xffffffffu, in.o, 1);  // next record's offset
+  if (lane == 31) o1 = in.f1;
+  const bool ok = b < nblk && e < n;
+  in.h = make_uint4(kSlotOverflow, 0u, 0u, 0u);
+  in.s1 = make_uint4(0u, 0u, 0u, 0u);
+  in.s2 = in.s1;
+  in.s3 = in.s1;
+  in.r = ok ? rec_sorted[e] : 0u;
+  if (ok && o1 > in.o) {  // the slot of a record without tiles is never written
+    const uint4* sl = slots + 4ull * e;
+    in.h = sl[0];
+    in.s1 = sl[1];
+    in.s2 = sl[2];
+    in.s3 = sl[3];
+  }
+}
+
+// PF: software pipeline over the warp's blocks (slots + payloads of the next
+// block and offsets of the one after are in flight while a block is written)
+template <int WB, bool PF = false>
 __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ rec_sorted,
                                                    const uint32_t* __restrict__ offs, uint32_t n,
                                                    uint32_t P, const uint4* __restrict__ slots,
@@ -807,22 +843,27 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
   uint32_t* s_ov = s_ot + WB;
   if (WB > 0)
     for (int i = lane; i < WB; i += 32) s_ot[i] = 0xFFFFFFFFu;  // sentinel: not ours
-  for (uint32_t b = blockIdx.x * 8u + (uint32_t)w; b < nblk; b += gridDim.x * 8u) {
+  const uint32_t bstep = gridDim.x * 8u;
+  EmitIn cur, nx;
+  if (PF) {
+    const uint32_t b0 = blockIdx.x * 8u + (uint32_t)w;
+    emit_load_offs(offs, n, P, nblk, b0, lane, cur);
+    emit_load_slots(rec_sorted, slots, n, nblk, b0, lane, cur);
+    emit_load_offs(offs, n, P, nblk, b0 + bstep, lane, nx);
+  }
+  for (uint32_t b = blockIdx.x * 8u + (uint32_t)w; b < nblk; b += bstep) {
     const uint32_t e = b * 32u + (uint32_t)lane;
     const bool ok = e < n;
-    const uint32_t o = ok ? offs[e] : P;
-    const uint32_t f1 = b * 32u + 32u < n ? offs[b * 32u + 32u] : P;
-    uint32_t o1 = __shfl_down_sync(0xffffffffu, o, 1);  // next record's offset
-    if (lane == 31) o1 = f1;
-    uint4 h = make_uint4(kSlotOverflow, 0u, 0u, 0u), s1 = make_uint4(0u, 0u, 0u, 0u), s2 = s1,
-          s3 = s1;
-    if (ok && o1 > o) {  // the slot of a record without tiles is never written
-      const uint4* sl = slots + 4ull * e;
-      h = sl[0];
-      s1 = sl[1];
-      s2 = sl[2];
-      s3 = sl[3];
+    if (PF) {  // issue the next block's slots and the offsets after it
+      emit_load_slots(rec_sorted, slots, n, nblk, b + bstep, lane, nx);
+    } else {
+      emit_load_offs(offs, n, P, nblk, b, lane, cur);
+      emit_load_slots(rec_sorted, slots, n, nblk, b, lane, cur);
     }
+    EmitIn nn;
+    if (PF) emit_load_offs(offs, n, P, nblk, b + 2 * bstep, lane, nn);
+    const uint32_t o = cur.o, f1 = cur.f1;
+    const uint4 h = cur.h, s1 = cur.s1, s2 = cur.s2, s3 = cur.s3;
     const bool dec = !(h.x & kSlotOverflow);  // fast record (big ones: k_emit_big)
     const int nrows = dec ? (int)((h.x >> 16) & 0xFFu) : 0;
     {  // stage the rows
@@ -841,7 +882,7 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
         q += (uint32_t)__popcll(mr[t]);
       }
       s_rb[w][lane] = (h.x & 0xFFFFu) * TX + h.y;
-      s_r[w][lane] = ok ? rec_sorted[e] : 0u;
+      s_r[w][lane] = ok ? cur.r : 0u;
     }
     int pre = nrows;  // warp inclusive prefix of row items
 #pragma unroll
@@ -905,6 +946,11 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
         }
       }
       __syncwarp();
+    }
+    if (PF) {
+      cur = nx;
+      nx.o = nn.o;
+      nx.f1 = nn.f1;
     }
   }
 }

@@ -145,3 +145,27 @@ def test_tile_split_equals_whole_tile_composite(W, H):
             imgs.append(g.render(cluster_size=4, output_format=fmt, rows=(2, 6)).cpu().numpy())
     for a, b in zip(imgs[:4], imgs[4:]):
         assert np.array_equal(a, b)
+
+
+def test_orbit_rig_bands_equal_full_frame():
+    # config C's display and orbit rig (narrow clusters: the per-axis
+    # rigid-motion bound pre-cull, and in bands the lazy-SH pre-test before
+    # the exact EWA) with a reduced scene_gen v1 scene: every band's sorted
+    # pairs are the full frame's filtered to its rows and the band images
+    # tile the full frame bit for bit
+    _need_gpu()
+    from paper_2605_04509_b200 import CoherentRaster
+    c = sy.CONFIGS["C"]
+    g = CoherentRaster(0)
+    g.upload_gaussians(sy.scene_gen_v1(200_000, 3, seed=3))
+    g.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset, c.view_cone)
+    g.set_camera_rig(c.make_rig())
+    full = g.render(8, output_format="rgb8").cpu().numpy()
+    kf, pf = g.sorted_pairs()
+    tf = (kf >> np.uint64(32 + 4)) // np.uint64(240)  # Bit_K = 4 (K = 13), TX = 240
+    for r0, r1 in [(0, 9), (40, 47), (66, 71), (120, 135)]:
+        band = g.render(8, output_format="rgb8", rows=(r0, r1)).cpu().numpy()
+        assert np.array_equal(band, full[r0 * 16:r1 * 16])
+        kb, pb = g.sorted_pairs()
+        sel = (tf >= r0) & (tf < r1)
+        assert np.array_equal(kb, kf[sel]) and np.array_equal(pb, pf[sel])

@@ -23,6 +23,7 @@ def run_a():
         g.render(s, stats=True)
     g.render(4, rows=(2, 6), output_format="float")
     g.render(1, fullframe=True)
+    g.render(1, fullframe=True, view_batch=3)
     g.render(8, kernel=1)
     g.render(8, remap=False, kernel=1)
     g.sorted_pairs()
