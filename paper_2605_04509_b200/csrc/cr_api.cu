@@ -298,31 +298,33 @@ cr_status radix_pass(cr_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
 // config C and 21.2 -> 20.3 ms at D against 16 items at 5 CTAs/SM; 12 items
 // at 6 CTAs/SM 3.70 ms; 20 items exceed the 48 KB static shared memory)
 constexpr int kOneItems = 18;
+// bits0 = 9: the first digit is 9 bits wide (512 buckets), so a 17-bit 8K
+// tile id takes 2 passes instead of 3.
 cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uint32_t*& vB,
                      long long n, int shift0, int npass, unsigned aggmask = 0,
-                     bool hist_ready = false, uint32_t slotK = 0) {
+                     bool hist_ready = false, uint32_t slotK = 0, int bits0 = 8) {
   if (n <= 0 || npass <= 0) return CR_OK;
   if (npass > 4) return fail(c, CR_ERR_CAPACITY, "radix_sort: npass %d > 4", npass);
   constexpr long long kTile = (long long)kSortThreads * kOneItems;
   const long long nb = (n + kTile - 1) / kTile;
-  CR_TRY(ensure(c, c->hist, (size_t)(4 * 256 + 16) * 4));
-  const size_t lbytes = (size_t)nb * 256 * 8;
+  CR_TRY(ensure(c, c->hist, (size_t)(4 * kHistBins + 16) * 4));
+  const size_t lbytes = (size_t)nb * (bits0 == 9 ? 512 : 256) * 8;
   if (lbytes > c->look.bytes || !c->look.p) {
     CR_TRY(ensure(c, c->look, lbytes));
     CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
     c->epoch = 0;
   }
   uint32_t* gh = P_<uint32_t>(c->hist);
-  uint32_t* ctr = gh + 4 * 256;
+  uint32_t* ctr = gh + 4 * kHistBins;
   if (hist_ready) {  // histograms already in c->hist (k_bin): zero only the tile counters
     CR_CUDA(c, cudaMemsetAsync(ctr, 0, 16 * 4, c->stream));
   } else {
-    CR_CUDA(c, cudaMemsetAsync(gh, 0, (4 * 256 + 16) * 4, c->stream));
+    CR_CUDA(c, cudaMemsetAsync(gh, 0, (4 * kHistBins + 16) * 4, c->stream));
   }
   const unsigned hgrid = (unsigned)std::max<long long>(
       1, std::min<long long>((n / 4 + kHistThreads - 1) / kHistThreads, 148 * 8));
   if (!hist_ready) {
-    k_radix_hist<<<hgrid, kHistThreads, 0, c->stream>>>(kA, n, shift0, npass, aggmask, gh);
+    k_radix_hist<<<hgrid, kHistThreads, 0, c->stream>>>(kA, n, shift0, npass, aggmask, gh, bits0);
     CR_LAUNCHED(c);
   }
   for (int p = 0; p < npass; ++p) {
@@ -330,9 +332,19 @@ cr_status radix_sort(cr_ctx* c, uint32_t*& kA, uint32_t*& vA, uint32_t*& kB, uin
       CR_CUDA(c, cudaMemsetAsync(c->look.p, 0, c->look.bytes, c->stream));
       c->epoch = 1;
     }
-    k_radix_onesweep<kOneItems, 7, 4><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
-        kA, vA, kB, vB, n, shift0 + 8 * p, gh + 256 * p, P_<unsigned long long>(c->look),
-        ctr + p, c->epoch, p == npass - 1 ? slotK : 0u);
+    const int sh = p == 0 ? shift0 : shift0 + bits0 + 8 * (p - 1);
+    if (p == 0 && bits0 == 9) {
+      constexpr int dyn = onesweep_dyn_smem<kOneItems>();
+      cudaFuncSetAttribute(k_radix_onesweep_n<kOneItems, 7, 3, 512>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      k_radix_onesweep_n<kOneItems, 7, 3, 512><<<(unsigned)nb, kSortThreads, dyn, c->stream>>>(
+          kA, vA, kB, vB, n, sh, gh + kHistBins * p, P_<unsigned long long>(c->look), ctr + p,
+          c->epoch, p == npass - 1 ? slotK : 0u);
+    } else {
+      k_radix_onesweep<kOneItems, 7, 4><<<(unsigned)nb, kSortThreads, 0, c->stream>>>(
+          kA, vA, kB, vB, n, sh, gh + kHistBins * p, P_<unsigned long long>(c->look), ctr + p,
+          c->epoch, p == npass - 1 ? slotK : 0u);
+    }
     CR_LAUNCHED(c);
     std::swap(kA, kB);
     std::swap(vA, vB);
@@ -1071,7 +1083,13 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     unsigned agg = 0;
     for (int sh = 8, q = 1; sh < tbits; sh += 8, ++q)
       if (((long long)(row1 - row0) * TX >> sh) < 64) agg |= 1u << q;
-    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, tpass, agg, false, (uint32_t)K));
+    // 17-bit (8K) tile ids: a 9-bit first digit makes it 2 passes (CR_EXP bit 3: 8-bit digits)
+    const int b0 = (tbits == 17 && !(c->exp & 8)) ? 9 : 8;
+    const int np = b0 == 9 ? 2 : tpass;
+    unsigned agg2 = 0;
+    for (int q = 1, sh = b0; sh < tbits; sh += 8, ++q)
+      if (((long long)(row1 - row0) * TX >> sh) < 64) agg2 |= 1u << q;
+    CR_TRY(radix_sort(c, tA, pA, tB, pB, P, 0, np, b0 == 9 ? agg2 : agg, false, (uint32_t)K, b0));
   }
   const size_t nSE = (size_t)TX * TY * K;
   CR_TRY(ensure(c, c->S, nSE * 4));

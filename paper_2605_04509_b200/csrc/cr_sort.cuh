@@ -384,16 +384,36 @@ __device__ __forceinline__ unsigned warp_peers8(uint32_t d, bool valid) {
   return peers;
 }
 
+// lanes holding the same 9-bit digit as this lane (valid lanes only)
+__device__ __forceinline__ unsigned warp_peers9(uint32_t d, bool valid) {
+  unsigned peers = warp_peers8(d, valid);
+  unsigned m;
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %1, 256;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+      "@!p not.b32 %0, %0;\n\t}"
+      : "=r"(m)
+      : "r"(d));
+  return peers & m;
+}
+
 constexpr int kHistThreads = 256;
-// global histograms of NPASS consecutive 8-bit digits (shift0, shift0+8, ...)
-// into ghist[pass][256] (zeroed by the caller).  aggmask bit p: digit p is
-// skewed (few distinct values) -> warp-aggregated counts.
+constexpr int kHistBins = 512;  // per pass in ghist: 256 bins, or 512 for a 9-bit first digit
+// global histograms of NPASS consecutive digits (the first bits0 = 8 or 9
+// bits wide at shift0, then 8-bit digits) into ghist[pass][kHistBins]
+// (zeroed by the caller).  aggmask bit p: digit p is skewed (few distinct
+// values) -> warp-aggregated counts.
+__device__ __forceinline__ int digit_shift(int shift0, int bits0, int p) {
+  return p == 0 ? shift0 : shift0 + bits0 + 8 * (p - 1);
+}
 __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __restrict__ keys,
                                                              long long n, int shift0, int npass,
                                                              unsigned aggmask,
-                                                             uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t s_h[4][256];
-  for (int q = threadIdx.x; q < 4 * 256; q += kHistThreads) (&s_h[0][0])[q] = 0;
+                                                             uint32_t* __restrict__ ghist,
+                                                             int bits0 = 8) {
+  __shared__ uint32_t s_h[4][kHistBins];
+  for (int q = threadIdx.x; q < 4 * kHistBins; q += kHistThreads) (&s_h[0][0])[q] = 0;
   __syncthreads();
   const long long n4 = n >> 2;
   const uint4* k4 = reinterpret_cast<const uint4*>(keys);
@@ -405,9 +425,10 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
     const bool ok = e < n4;
     const uint4 v = ok ? k4[e] : make_uint4(0, 0, 0, 0);
     for (int p = 0; p < npass; ++p) {
-      const int sh = shift0 + 8 * p;
-      const uint32_t d0 = (v.x >> sh) & 255u, d1 = (v.y >> sh) & 255u;
-      const uint32_t d2 = (v.z >> sh) & 255u, d3 = (v.w >> sh) & 255u;
+      const int sh = digit_shift(shift0, bits0, p);
+      const uint32_t dm = (p == 0 && bits0 == 9) ? 511u : 255u;
+      const uint32_t d0 = (v.x >> sh) & dm, d1 = (v.y >> sh) & dm;
+      const uint32_t d2 = (v.z >> sh) & dm, d3 = (v.w >> sh) & dm;
       if ((aggmask >> p) & 1u) {
         // run-aggregate the 4 keys, then across the warp
         const bool same = ok && d0 == d1 && d0 == d2 && d0 == d3;
@@ -417,7 +438,7 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
           atomicAdd(&s_h[p][d2], 1u);
           atomicAdd(&s_h[p][d3], 1u);
         }
-        const unsigned peers = warp_peers8(d0, same);
+        const unsigned peers = dm == 511u ? warp_peers9(d0, same) : warp_peers8(d0, same);
         if (same && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
           atomicAdd(&s_h[p][d0], 4u * (uint32_t)__popc(peers));
       } else if (ok) {
@@ -431,10 +452,11 @@ __global__ void __launch_bounds__(kHistThreads) k_radix_hist(const uint32_t* __r
   // tail (n % 4) in block 0
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
     const uint32_t k = keys[(n4 << 2) + threadIdx.x];
-    for (int p = 0; p < npass; ++p) atomicAdd(&s_h[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+    for (int p = 0; p < npass; ++p)
+      atomicAdd(&s_h[p][(k >> digit_shift(shift0, bits0, p)) & ((p == 0 && bits0 == 9) ? 511u : 255u)], 1u);
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < npass * 256; q += kHistThreads) {
+  for (int q = threadIdx.x; q < npass * kHistBins; q += kHistThreads) {
     const uint32_t c = (&s_h[0][0])[q];
     if (c) atomicAdd(&ghist[q], c);
   }
@@ -569,6 +591,162 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_radix_onesweep(
   for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
     const uint32_t k = s_k[p], v = s_v[p];
     const uint32_t gp = s_off[(k >> shift) & 255u] + (uint32_t)p;
+    vals_out[gp] = v;
+    keys_out[gp] = slotK ? k * slotK + fdiv(v, c_fp.divM) : k;
+  }
+}
+
+template <int ITEMS, bool FULL, bool VALS, int NDIG>
+__device__ __forceinline__ void onesweep_rank_n(const uint32_t* __restrict__ keys,
+                                              const uint32_t* __restrict__ vals, long long n,
+                                              long long wbase, int shift, int lane, unsigned lt,
+                                              uint32_t* s_cw, uint32_t* kr, uint32_t* vr,
+                                              uint32_t* dl) {
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const long long e = wbase + q * 32 + lane;
+    const bool ok = FULL || e < n;
+    kr[q] = ok ? keys[e] : 0u;
+    if (VALS) vr[q] = ok ? vals[e] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const bool ok = FULL || wbase + q * 32 + lane < n;
+    const uint32_t d = ok ? ((kr[q] >> shift) & (uint32_t)(NDIG - 1)) : (uint32_t)NDIG;
+    unsigned peers;
+    if (NDIG == 512) peers = FULL ? warp_peers9(d, true) : warp_peers9(d, ok);
+    else peers = FULL ? warp_peers8(d, true) : warp_peers8(d, ok);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (ok && lane == leader) old = atomicAdd(&s_cw[d], (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
+    dl[q] = d | ((old + __popc(peers & lt)) << 10);
+  }
+}
+
+// The same pass for NDIG = 512 (a 9-bit digit: the first pass of a 17-bit
+// 8K tile sort, which then takes 2 passes instead of 3), each thread owning
+// NDIG / 256 digits; key / value staging in dynamic shared memory.  (Kept
+// apart from the 8-bit kernel above, which the generic form slows by 1 %.)
+template <int ITEMS>
+constexpr int onesweep_dyn_smem() { return 2 * kSortThreads * ITEMS * 4; }
+template <int ITEMS, int VAR, int MINB = 3, int NDIG = 256>
+__global__ void __launch_bounds__(kSortThreads, MINB) k_radix_onesweep_n(
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, long long n, int shift,
+    const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ look,
+    uint32_t* __restrict__ ctr, uint32_t epoch, uint32_t slotK) {
+  constexpr int TILE = kSortThreads * ITEMS;
+  constexpr bool LATE = (VAR & 2) != 0;
+  constexpr int DPT = NDIG / kSortThreads;  // digits per thread
+  constexpr uint32_t DM = NDIG - 1;
+  __shared__ uint32_t s_cnt[kSortWarps][NDIG];  // counts -> block-local warp offsets
+  __shared__ uint32_t s_off[NDIG];              // global base - block-local offset
+  __shared__ uint32_t s_kv_st[NDIG == 256 ? 2 * TILE : 1];
+  extern __shared__ uint32_t s_kv_dyn[];
+  uint32_t* s_k = NDIG == 256 ? s_kv_st : s_kv_dyn;
+  uint32_t* s_v = s_k + TILE;
+  __shared__ uint32_t s_ws[2][kSortWarps];
+  __shared__ uint32_t s_bid;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x == 0) s_bid = atomicAdd(ctr, 1u);
+  for (int q = threadIdx.x; q < kSortWarps * NDIG; q += kSortThreads) (&s_cnt[0][0])[q] = 0;
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const long long bbase = (long long)bid * TILE;
+  const long long wbase = bbase + (long long)w * (ITEMS * 32);
+  uint32_t kr[ITEMS], vr[ITEMS], dl[ITEMS];  // dl = digit | rank << 10
+  constexpr bool VALS = (VAR & 4) == 0;  // bit 2: values loaded at the scatter
+  if ((VAR & 1) && bbase + TILE <= n)
+    onesweep_rank_n<ITEMS, true, VALS, NDIG>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
+  else
+    onesweep_rank_n<ITEMS, false, VALS, NDIG>(keys, vals, n, wbase, shift, lane, lt, s_cnt[w], kr, vr, dl);
+  __syncthreads();
+  const unsigned long long hiA = (unsigned long long)((epoch << 2) | 1u) << 32;
+  const unsigned long long hiP = (unsigned long long)((epoch << 2) | 2u) << 32;
+  uint32_t acc[DPT], gh[DPT], loff[DPT], goff[DPT];
+#pragma unroll
+  for (int h = 0; h < DPT; ++h) {
+    const int d = h * kSortThreads + threadIdx.x;
+    uint32_t a = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = s_cnt[ww][d];
+      s_cnt[ww][d] = a;
+      a += c;
+    }
+    acc[h] = a;
+    // publish this tile's count of digit d as early as possible
+    st_status(look + (size_t)bid * NDIG + d, (bid == 0 ? hiP : hiA) | a);
+    gh[h] = ghist[d];
+  }
+  // block-local digit offsets and global digit starts (two NDIG-wide scans)
+  uint32_t c1 = 0, c2 = 0;
+#pragma unroll
+  for (int h = 0; h < DPT; ++h) {
+    uint32_t i1 = acc[h], i2 = gh[h];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y1 = __shfl_up_sync(0xffffffffu, i1, o);
+      const uint32_t y2 = __shfl_up_sync(0xffffffffu, i2, o);
+      if (lane >= o) { i1 += y1; i2 += y2; }
+    }
+    if (lane == 31) { s_ws[0][w] = i1; s_ws[1][w] = i2; }
+    __syncthreads();
+    uint32_t p1 = 0, p2 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      if (ww < w) { p1 += s_ws[0][ww]; p2 += s_ws[1][ww]; }
+      t1 += s_ws[0][ww];
+      t2 += s_ws[1][ww];
+    }
+    loff[h] = c1 + p1 + i1 - acc[h];
+    goff[h] = c2 + p2 + i2 - gh[h];
+    c1 += t1;
+    c2 += t2;
+    if (DPT > 1) __syncthreads();  // s_ws is reused by the next digit group
+  }
+  // look back for the exclusive prefix of digit d over the preceding tiles
+  uint32_t excl[DPT];
+#pragma unroll
+  for (int h = 0; h < DPT; ++h) {
+    const int d = h * kSortThreads + threadIdx.x;
+    excl[h] = 0;
+    if (!LATE && bid > 0) {
+      excl[h] = lookback4(look + (size_t)(bid - 1) * NDIG + d, (long long)bid, NDIG, epoch);
+      st_status(look + (size_t)bid * NDIG + d, hiP | (excl[h] + acc[h]));
+    }
+    if (!LATE) s_off[d] = goff[h] + excl[h] - loff[h];
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) s_cnt[ww][d] += loff[h];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    const uint32_t dq = dl[q] & 1023u;
+    if (dq < (uint32_t)NDIG) {
+      const uint32_t p = s_cnt[w][dq] + (dl[q] >> 10);
+      s_v[p] = VALS ? vr[q] : vals[wbase + q * 32 + lane];
+      s_k[p] = kr[q];
+    }
+  }
+  if (LATE) {
+#pragma unroll
+    for (int h = 0; h < DPT; ++h) {
+      const int d = h * kSortThreads + threadIdx.x;
+      if (bid > 0) {
+        excl[h] = lookback4(look + (size_t)(bid - 1) * NDIG + d, (long long)bid, NDIG, epoch);
+        st_status(look + (size_t)bid * NDIG + d, hiP | (excl[h] + acc[h]));
+      }
+      s_off[d] = goff[h] + excl[h] - loff[h];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)min((long long)TILE, n - bbase);
+  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
+    const uint32_t k = s_k[p], v = s_v[p];
+    const uint32_t gp = s_off[(k >> shift) & DM] + (uint32_t)p;
     vals_out[gp] = v;
     keys_out[gp] = slotK ? k * slotK + fdiv(v, c_fp.divM) : k;
   }

@@ -169,3 +169,37 @@ def test_orbit_rig_bands_equal_full_frame():
         kb, pb = g.sorted_pairs()
         sel = (tf >= r0) & (tf < r1)
         assert np.array_equal(kb, kf[sel]) and np.array_equal(pb, pf[sel])
+
+
+def test_17bit_tile_ids_nine_bit_first_pass():
+    # 8192 x 2064 px = 512 x 129 tiles: 17-bit tile ids, sorted in 2 passes
+    # with a 9-bit first digit; bit-identical to 3 passes of 8-bit digits
+    # (CR_EXP bit 3), and a band of it against the oracle
+    _need_gpu()
+    import os
+    from paper_2605_04509_b200 import CoherentRaster
+    W, H, N = 8192, 2064, 6
+    sc = sy.random_scene(20000, 1, seed=53, scale_median=0.03)
+    cams = sy.orbit_rig(N, 6.0, W, H, radius=3.0, height=0.2, fov_y_deg=40.0)
+    res = []
+    for exp in ("0", "8"):
+        old = os.environ.get("CR_EXP")
+        os.environ["CR_EXP"] = exp
+        try:
+            g = CoherentRaster(0)
+        finally:
+            if old is None:
+                del os.environ["CR_EXP"]
+            else:
+                os.environ["CR_EXP"] = old
+        g.upload_gaussians(sc)
+        g.set_display(W, H, N, 13.3, 0.17, 2.1)
+        g.set_camera_rig(cams)
+        img = g.render(3, output_format="rgb8", stats=True).cpu().numpy()
+        k, p = g.sorted_pairs()
+        res.append((img, k, p, g.last_stats["pairs"]))
+    assert res[0][3] == res[1][3] > 100000
+    for a, b in zip(res[0][:3], res[1][:3]):
+        assert np.array_equal(a, b)
+    g, o = make_pair(sc, W, H, N, 13.3, 0.17, 2.1, cams)
+    check_frame(g, o, 3, rows=(60, 64))
