@@ -1,4 +1,5 @@
-"""Two CR_EXP developer switches render bit-identical frames (float and RGB8):
+"""Two CR_EXP developer switches render bit-identical frames (float and RGB8)
+and sorted (key, payload) pairs:
 python tools/exp_equal.py C 0 4 [s]"""
 import os, subprocess, sys
 cfg, ea, eb = sys.argv[1], sys.argv[2], sys.argv[3]
@@ -18,7 +19,9 @@ h = hashlib.sha1()
 for fmt in ("float", "rgb8"):
     h.update(r.render(s, output_format=fmt).cpu().numpy().tobytes())
 r.render(s, stats=True, count_evals=True)
-print(h.hexdigest(), r.last_stats["evals"])
+k, p = r.sorted_pairs()
+h.update(k.tobytes()); h.update(p.tobytes())
+print(h.hexdigest(), r.last_stats["evals"], r.last_stats["pairs"])
 '''
 outs = []
 for e in (ea, eb):
