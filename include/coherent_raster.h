@@ -59,6 +59,10 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out);
 void cr_destroy(cr_ctx* ctx);
 /* Re-bind the stream used by subsequent calls. */
 cr_status cr_set_stream(cr_ctx* ctx, void* cuda_stream);
+/* Wait until every frame this context has rendered is complete, including
+ * the host copies of CR_FLAG_ASYNC_OUT renders (their host buffers may be
+ * read after this returns). */
+cr_status cr_synchronize(cr_ctx* ctx);
 /* Context-owned diagnostic of the last failing call (valid until the next call). */
 const char* cr_last_error(const cr_ctx* ctx);
 const char* cr_status_string(cr_status s);
@@ -159,6 +163,13 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  *                  CR_FLAG_VIEW_FRAMES (implies the full-frame render) returns
  *                  those per-view frames instead of interlacing them: out is
  *                  [N][rows][W][3], out_bytes >= N times the band size.
+ *                  CR_FLAG_ASYNC_OUT (host `out` only, interlaced frame): the
+ *                  frame is copied to `out` on the context's copy stream after
+ *                  the composite (two device staging buffers, so the copy of
+ *                  frame n overlaps the rendering of frame n+1) and the call
+ *                  returns without waiting; `out` must stay valid and unread
+ *                  until cr_synchronize (pinned memory makes the copy
+ *                  asynchronous).  Ignored with stats (they synchronise).
  *   view_batch     full-frame render only: views per pass (the paper's
  *                  "3DGS (batch=B)" baseline, T2 P:520; 1 = plain
  *                  per-view 3DGS): the N views are rendered B at a time, each
@@ -175,6 +186,7 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
 #define CR_FLAG_COUNT_EVALS 1
 #define CR_FLAG_FULLFRAME 2
 #define CR_FLAG_VIEW_FRAMES 4
+#define CR_FLAG_ASYNC_OUT 8
 typedef struct {
   int32_t cluster_size;
   int32_t remap;

@@ -19,7 +19,7 @@ STATUS = {
 
 # exported symbols, in header order (tests check the library exports all of them)
 SYMBOLS = [
-    "cr_create", "cr_destroy", "cr_set_stream", "cr_last_error", "cr_status_string", "cr_version",
+    "cr_create", "cr_destroy", "cr_set_stream", "cr_synchronize", "cr_last_error", "cr_status_string", "cr_version",
     "cr_upload_gaussians", "cr_set_display", "cr_set_camera_rig", "cr_make_orbit_rig",
     "cr_render_interlaced", "cr_get_view_map", "cr_get_remap", "cr_get_sorted_pairs",
     "cr_get_ranges", "cr_get_depths", "cr_get_counts",
@@ -87,6 +87,7 @@ def load(path: str | None = None):
     sig("cr_create", st, C.c_int, vp, C.POINTER(vp))
     sig("cr_destroy", None, vp)
     sig("cr_set_stream", st, vp, vp)
+    sig("cr_synchronize", st, vp)
     sig("cr_last_error", C.c_char_p, vp)
     sig("cr_status_string", C.c_char_p, st)
     sig("cr_version", C.c_char_p)

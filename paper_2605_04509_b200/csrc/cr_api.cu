@@ -137,6 +137,11 @@ struct cr_ctx {
   cudaStream_t side = nullptr;     // forked stream for concurrent big-record emission
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_batch[2] = {};    // around a batched full-frame render
+  // CR_FLAG_ASYNC_OUT: double-buffered device staging, copies on their own stream
+  DevBuf astage[2];
+  int aslot = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_comp[2] = {}, ev_copy[2] = {};
   long long device_bytes = 0;
   bool debug = false;  // CR_DEBUG=1: synchronise + trace after every stage
   int exp = 0;         // CR_EXP (read once at cr_create): developer A/B switches, 0 = shipped path
@@ -438,6 +443,11 @@ cr_status cr_create(int cuda_device, void* cuda_stream, cr_ctx** out) {
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   for (auto& e : c->ev_batch) cudaEventCreate(&e);
+  for (int q = 0; q < 2; ++q) {
+    cudaEventCreateWithFlags(&c->ev_comp[q], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_copy[q], cudaEventDisableTiming);
+  }
+  cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
@@ -463,6 +473,15 @@ void cr_destroy(cr_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ev_batch)
     if (e) cudaEventDestroy(e);
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (c->ev_comp[q]) cudaEventDestroy(c->ev_comp[q]);
+    if (c->ev_copy[q]) cudaEventDestroy(c->ev_copy[q]);
+    release(c->astage[q]);
+  }
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
@@ -471,6 +490,14 @@ void cr_destroy(cr_ctx* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
+}
+
+cr_status cr_synchronize(cr_ctx* c) {
+  if (!c) return CR_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  CR_CUDA(c, cudaStreamSynchronize(c->stream));
+  CR_CUDA(c, cudaStreamSynchronize(c->copy));
+  return CR_OK;
 }
 
 cr_status cr_set_stream(cr_ctx* c, void* s) {
@@ -1106,7 +1133,13 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
 
   // ---- a9 composite
   void* dst = out;
-  if (!out_on_device) {
+  const bool async_out = !out_on_device && !st && !fullframe && (o->flags & CR_FLAG_ASYNC_OUT);
+  const int aslot = c->aslot;
+  if (async_out) {  // this slot's previous host copy must be done before it is rewritten
+    CR_TRY(ensure(c, c->astage[aslot], obytes));
+    CR_CUDA(c, cudaStreamWaitEvent(str, c->ev_copy[aslot], 0));
+    dst = c->astage[aslot].p;
+  } else if (!out_on_device) {
     CR_TRY(ensure(c, c->stage_out, obytes));
     dst = c->stage_out.p;
   }
@@ -1165,7 +1198,13 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_LAUNCHED(c);
   CR_TRACE(c, "composite");
   CR_CUDA(c, cudaEventRecord(c->ev[5], str));
-  if (!out_on_device) {
+  if (async_out) {  // D2H on the copy stream, overlapping the next frame's kernels
+    CR_CUDA(c, cudaEventRecord(c->ev_comp[aslot], str));
+    CR_CUDA(c, cudaStreamWaitEvent(c->copy, c->ev_comp[aslot], 0));
+    CR_CUDA(c, cudaMemcpyAsync(out, dst, obytes, cudaMemcpyDeviceToHost, c->copy));
+    CR_CUDA(c, cudaEventRecord(c->ev_copy[aslot], c->copy));
+    c->aslot = aslot ^ 1;
+  } else if (!out_on_device) {
     CR_CUDA(c, cudaMemcpyAsync(out, dst, obytes, cudaMemcpyDeviceToHost, str));
     CR_CUDA(c, cudaStreamSynchronize(str));
   }

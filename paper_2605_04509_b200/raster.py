@@ -70,6 +70,10 @@ class CoherentRaster:
         self._stream = stream
         self._check(self._L.cr_set_stream(self._ctx, C.c_void_p(stream.cuda_stream)))
 
+    def synchronize(self):
+        """Wait for every rendered frame, including async_out host copies."""
+        self._check(self._L.cr_synchronize(self._ctx))
+
     @staticmethod
     def version() -> str:
         return N.load().cr_version().decode()
@@ -132,7 +136,7 @@ class CoherentRaster:
     def render(self, cluster_size: int = 8, remap: bool = True, kernel: int | None = None,
                background=(0.0, 0.0, 0.0), output_format: str = "rgb8", rows=None, out=None,
                stats: bool = False, count_evals: bool = False, fullframe: bool = False,
-               view_frames: bool = False, view_batch: int = 0):
+               view_frames: bool = False, view_batch: int = 0, async_out: bool = False):
         """One interlaced frame I_LF (Alg.1) for tile rows `rows`
         (None = full frame).  Returns a CUDA tensor [rows*16, W, 3] (uint8 or
         float32); `out` may be a preallocated CUDA tensor or a host tensor /
@@ -141,7 +145,9 @@ class CoherentRaster:
         traditional baseline).  view_frames=True returns those per-view frames
         [N, rows*16, W, 3] instead (the per-view images of P:478).
         view_batch=B renders the full-frame baseline B views per pass (the
-        paper's "3DGS (batch=B)"; 1 = plain per-view 3DGS)."""
+        paper's "3DGS (batch=B)"; 1 = plain per-view 3DGS).
+        async_out=True with a host `out` (pinned): the copy back overlaps the
+        next frame; `out` is valid after synchronize()."""
         if kernel is None:
             kernel = 0 if remap else 1
         fmt = 0 if output_format == "rgb8" else 1
@@ -149,7 +155,7 @@ class CoherentRaster:
         opts = N.RenderOpts(int(cluster_size), int(bool(remap)), int(kernel),
                             (C.c_float * 3)(*[float(b) for b in background]), fmt, int(r0), int(r1),
                             (1 if count_evals else 0) | (2 if fullframe else 0)
-                            | (4 if view_frames else 0), int(view_batch))
+                            | (4 if view_frames else 0) | (8 if async_out else 0), int(view_batch))
         dtype = torch.uint8 if fmt == 0 else torch.float32
         if self.display is None:  # let the library report CR_ERR_NOT_READY
             out = torch.empty(1, dtype=dtype, device=self.device) if out is None else out

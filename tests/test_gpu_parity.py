@@ -467,3 +467,24 @@ def test_paper_display_panels_sampled_tiles(name):
     tiles = np.unique(np.concatenate([rng.choice(TX * TY, 16, replace=False),
                                       (TY // 2) * TX + rng.integers(0, TX, 8)])).astype(np.int32)
     _sampled_tile_check(g, o, c, c.cluster_size, tiles)
+
+
+def test_async_host_output(cfgA_pair):
+    # CR_FLAG_ASYNC_OUT: frames copied to pinned host buffers on the copy
+    # stream (double-buffered device staging) equal the synchronous renders
+    g, o = cfgA_pair
+    c = sy.CONFIGS["A"]
+    rigs = [c.make_rig(), sy.orbit_rig(c.N, 6.0, c.W, c.H, radius=3.2, height=0.1, fov_y_deg=50.0),
+            c.make_rig()]
+    ref = []
+    for cams in rigs:
+        g.set_camera_rig(cams)
+        ref.append(g.render(4, output_format="rgb8").cpu().numpy())
+    hosts = [torch.empty(g.band_shape(None), dtype=torch.uint8, pin_memory=True) for _ in rigs]
+    for cams, h in zip(rigs, hosts):
+        g.set_camera_rig(cams)
+        g.render(4, output_format="rgb8", out=h.numpy(), async_out=True)
+    g.synchronize()
+    for h, r_ in zip(hosts, ref):
+        assert np.array_equal(h.numpy(), r_)
+    g.set_camera_rig(c.make_rig())
