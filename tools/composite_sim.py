@@ -53,7 +53,7 @@ def main():
                P2_it=0, P2_stage=0, P2_stage_views=0, sub=0, evals=0, visits_ideal=0,
                A_nosat_it=0, visits_nosat=0, V1_it=0, V1_stage=0, A_union_it=0,
                Ay2_it=0, Ay2_masks=0, Aq4_it=0, Aq4_masks=0, H2_it=0, H2_masks=0, H2_stage=0,
-               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0)
+               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0, R_it=0, R_stage=0, R_stage_views=0)
     for t in tiles:
         tx, ty = t % TX, t // TX
         ls = psi[t]
@@ -163,6 +163,18 @@ def main():
                 for SB, key in ((64, "VL64_it"), (128, "VL128_it")):
                     for b in range(0, last, SB):
                         tot[key] += int(passm[:, b:b + SB].sum(1).max())
+            # ---- R: per 32-entry batch, the cluster's not-yet-saturated
+            # subpixels repacked (Psi order) into ceil(alive / 32) warps
+            last_all = int(stop.max())
+            for b in range(0, last_all, 32):
+                alive = np.nonzero(stop > b)[0]
+                for c0 in range(0, alive.size, 32):
+                    mem = alive[c0:c0 + 32]
+                    bx = boxes(mem)
+                    tot["R_stage"] += 1
+                    tot["R_stage_views"] += len(bx)
+                    pm = np.stack([bx[js[q]][b:b + 32] & (idx[b:b + 32] < stop[q]) for q in mem])
+                    tot["R_it"] += int(pm.sum(1).max())
             # ---- H2: chunks = the top / bottom half of the tile (<= 32 ranks each,
             # overflow split), per-view boxes inside the chunk (and per quadrant)
             half = (ys % 16 >= 8).astype(np.int64)
@@ -217,7 +229,8 @@ def main():
           f"util {tot['visits_nosat']/32/tot['A_nosat_it']:.3f}")
     print(f"masks: A {tot['A_stage_views']} y2 {tot['Ay2_masks']} q4 {tot['Aq4_masks']} stripe {tot['As_masks']}")
     print(f"H2 masks {tot['H2_masks']} stage {tot['H2_stage']}  H2q masks {tot['H2q_masks']}")
-    for k in ("VL64_it", "VL128_it", "P2_it", "V1_it", "A_union_it", "Ay2_it", "Aq4_it", "H2_it", "H2q_it", "As_it"):
+    print(f"repack: stage batches {tot['R_stage']} (views {tot['R_stage_views']}) vs A {tot['A_stage']} (views {tot['A_stage_views']})")
+    for k in ("R_it", "VL64_it", "VL128_it", "P2_it", "V1_it", "A_union_it", "Ay2_it", "Aq4_it", "H2_it", "H2q_it", "As_it"):
         print(f"{k}: {tot[k]} ({tot[k]/A:.3f} of A)")
     print(f"stage batches A {tot['A_stage']} (views {tot['A_stage_views']}), P2 {tot['P2_stage']} "
           f"(views {tot['P2_stage_views']})")
