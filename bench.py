@@ -52,6 +52,36 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def measure_traffic(cfg_name: str, s: int, kernel_regex: str = "k_composite_staged"):
+    """DRAM bytes (read + write) of one launch of the dominant kernel, from an
+    ncu capture of one frame of the same config in a subprocess (after the
+    timed region; ncu's replay never touches the timed numbers).  None when
+    ncu is unavailable or not permitted on this box."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control",
+           "none", "-k", "regex:" + kernel_regex, "-c", "1", "--csv",
+           sys.executable, os.path.join(ROOT, "tools", "prof_frame.py"), cfg_name, "1", str(s)]
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+    except Exception:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot, seen = 0.0, 0
+    for row in csv.reader(io.StringIO(res.stdout)):
+        if len(row) > 3 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                tot += float(row[-1].replace(",", "")) * scale.get(row[-2], 1.0)
+                seen += 1
+            except ValueError:
+                pass
+    return tot if seen == 2 else None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -205,6 +235,8 @@ def main():
     ap.add_argument("--no-remap", action="store_true")
     ap.add_argument("--kernel", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the ncu DRAM-traffic capture of the composite")
     ap.add_argument("--no-fullframe", action="store_true", help="skip the N1 full-frame comparator")
     ap.add_argument("--ref-rows", type=int, default=None,
                     help="oracle sample: tile rows (default 12 for cpu_baseline, 4 per --impl reference step)")
@@ -482,6 +514,9 @@ def main():
     mufu_peak = 148 * 16 * sm_max * 1e6 / 1e12
     mufu_ach = evals * MUFU_PER_EVAL / (comp_ms * 1e-3) / 1e12 if comp_ms > 0 else None
     bc = compulsory_bytes(cfg, info) if world == 1 else None
+    # the composite's DRAM bytes per launch (ncu subprocess, after the timed region)
+    traffic = (measure_traffic(args.config, cfg.cluster_size)
+               if world == 1 and not args.no_traffic and not pose_mode else None)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rows_s = (TY // 2 - args.ref_rows // 2, TY // 2 - args.ref_rows // 2 + args.ref_rows)
@@ -507,7 +542,7 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_composite_staged",
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-                     "traffic": None,
+                     "traffic": traffic,
                      "mufu": {"achieved": mufu_ach, "peak": mufu_peak, "unit": "T exp/s",
                               "frac": (mufu_ach / mufu_peak) if mufu_ach else None},
                      "note": (f"{FLOPS_PER_EVAL} algorithmic FP32 ops + {MUFU_PER_EVAL} MUFU exp "
@@ -515,8 +550,11 @@ def main():
                               "evaluations (the paper's traversal length, counted live by an "
                               "instrumented frame) / the composite's CUDA-event time in this "
                               f"run; peaks derived for {sm_max:.0f} MHz: 148 SM x 128 FP32 lanes "
-                              "x 2 and 148 SM x 16 SFU lanes (DESIGN.md §5); DRAM traffic per "
-                              "launch is not measured in this run (ncu captures: profiles/)")},
+                              "x 2 and 148 SM x 16 SFU lanes (DESIGN.md §5); traffic = DRAM "
+                              "bytes read + written by one composite launch, ncu on one frame of "
+                              "this config in a subprocess after the timed region (null: ncu "
+                              "unavailable); algorithmic bytes per launch ~7.7 GB at C "
+                              "(DESIGN.md §5)")},
         "frame_hbm": ({"compulsory_bytes": bc, "achieved_gbs": bc / (ms_per * 1e-3) / 1e9,
                        "peak_gbs": peaks.get("hbm_gbs"), "peak_source": peaks_src,
                        "frac": bc / (ms_per * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
