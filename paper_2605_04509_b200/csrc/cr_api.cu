@@ -107,8 +107,8 @@ struct cr_ctx {
   cr_display disp{};
   int TX = 0, TY = 0;
   DevBuf V, psi;
-  int chunks_s = -1, chunk_stride = 0;
-  DevBuf chunks, nchunks;
+  int chunks_s = -1, chunk_stride = 0, chunks_pairs = -1;
+  DevBuf chunks, nchunks, psi2;  // composite work items (psi2: paired-subpixel order)
   // rig
   bool has_rig = false;
   std::vector<CamDev> cams;
@@ -463,7 +463,7 @@ void cr_destroy(cr_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks,
+  DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks, &c->psi2,
                    &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->bigcnt,
                    &c->bigmask, &c->bigwlo, &c->biginfo, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->hist, &c->look, &c->slook,
@@ -898,15 +898,26 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_CUDA(c, cudaMemcpyToSymbolAsync(c_fp, &fp, sizeof(fp), 0, cudaMemcpyHostToDevice, str));
 
   // ---- composite work items (static per display and s)
-  if (o->kernel == 0 && !fullframe && c->chunks_s != s) {
+  // two subpixels of one view per lane (k_composite_pairs, the default); CR_EXP
+  // bit 6: one subpixel per lane (k_composite_staged, round 2's kernel)
+  const int pairs = (c->exp & 64) ? 0 : 1;
+  if (o->kernel == 0 && !fullframe && (c->chunks_s != s || c->chunks_pairs != pairs)) {
     const int stride = K + 24;
     CR_TRY(ensure(c, c->chunks, (size_t)TX * TY * stride * 4));
     CR_TRY(ensure(c, c->nchunks, (size_t)TX * TY * 4));
-    k_chunks_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
-        P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),
-        P_<uint32_t>(c->nchunks), stride, W, TX, TY, s);
+    if (pairs) {
+      CR_TRY(ensure(c, c->psi2, (size_t)TX * TY * kPairSlots * 2));
+      k_pairs_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
+          P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint16_t>(c->psi2), P_<uint32_t>(c->chunks),
+          P_<uint32_t>(c->nchunks), stride, W, TX, TY, s, (c->exp & 2048) ? 0 : 1);
+    } else {
+      k_chunks_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
+          P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),
+          P_<uint32_t>(c->nchunks), stride, W, TX, TY, s);
+    }
     CR_LAUNCHED(c);
     c->chunks_s = s;
+    c->chunks_pairs = pairs;
     c->chunk_stride = stride;
   }
 
@@ -1157,7 +1168,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),                       \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
       P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals, tsplit)
-#define CR_STAGED(F, CNT) CR_STAGED1(F, CNT, 0)
+#define CR_PAIRS(F, CNT)                                                                      \
+  k_composite_pairs<F, CNT, kCompWarps><<<ntile * tsplit, kCompWarps * 32, 0, str>>>(          \
+      P_<uint8_t>(c->V), P_<uint16_t>(c->psi2), P_<uint32_t>(c->chunks),                      \
+      P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
+      P_<float4>(c->rec0), m4, dst, evals, tsplit)
+#define CR_STAGED(F, CNT) do { if (pairs) CR_PAIRS(F, CNT); else CR_STAGED1(F, CNT, 0); } while (0)
 #define CR_THREAD(F, CNT)                                                                     \
   k_composite_thread<F, CNT><<<ntile, kTileSub, 0, str>>>(                                    \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA,    \
@@ -1193,6 +1209,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     else          { if (count) CR_THREAD(1, true); else CR_THREAD(1, false); }
   }
 #undef CR_STAGED
+#undef CR_PAIRS
 #undef CR_STAGED1
 #undef CR_THREAD
   CR_LAUNCHED(c);

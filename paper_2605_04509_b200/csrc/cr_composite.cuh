@@ -1,7 +1,9 @@
 // cr_composite.cuh — a9 subpixel compositing (Eqs.9-10; Alg.2
 // Alpha-Blend).
 //
-// k_composite_staged (B200 design, default):
+// k_composite_pairs (default) is the design below with two subpixels of one
+// view per lane and packed fp32x2 blend arithmetic (see its comment);
+// k_composite_staged (round 2's kernel, CR_EXP bit 6) is kept for A/B:
 //   CTA per 16x16 tile, 8 warps pulling "cluster-aligned warp chunks" (<= 32
 //   consecutive Psi ranks of one cluster k) from a shared-memory queue.  Per
 //   chunk the warp streams list (t,k) in 32-entry batches: lane l gathers
@@ -350,6 +352,240 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP_MINB) k_composite_staged(
           const long long o = ((long long)(y - c_fp.row0 * 16) * W + x) * 3 + u;
           if (FMT == 0) ((uint8_t*)out)[o] = (uint8_t)quant_u8(v);
           else ((float*)out)[o] = v;
+        }
+      }
+    }
+  }
+  if (COUNT) add_evals(evals, nev);
+  if (tsplit == 1) {
+    __syncthreads();
+    store_tile<FMT>(s_out, out, tx, ty, W, H, c_fp.row0 * 16);
+  }
+}
+
+// ===========================================================================
+// k_composite_pairs — the staged design with TWO subpixels of one view per
+// lane (k_pairs_build: view runs padded to even length, chunks of <= 32 slot
+// pairs), so one staged batch, one per-view cull mask and one walk serve twice
+// the subpixels, and the blend arithmetic of the two runs as packed fp32x2
+// instructions (FADD2 / FMUL2 / FFMA2, sm_100a), each half rounding exactly
+// like blend_step's scalar op (same operations, same order: frames are bit
+// identical to k_composite_staged).  A subpixel that saturates stops blending
+// (its weight is selected to 0 and T kept); the lane leaves the walk when both
+// have.
+// ===========================================================================
+
+__device__ __forceinline__ unsigned bit_at(int q) {  // 1u << q in one BMSK
+  unsigned r;
+  asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(r) : "r"(q));
+  return r;
+}
+
+#ifndef CR_COMP2_MINB
+#define CR_COMP2_MINB 10  // 48 registers: 10 CTAs x 4 warps per SM (measured: 11 -> 40 regs spills)
+#endif
+template <int NW>
+struct PairStage {  // one warp's staging area (rec / col share the entry offset 16 q)
+  float4 rec[32];
+  float4 col[32];          // (r, g, b, extents): a lane's colour is at rec + 512 + 4 u
+  float2 mu[kSlots * 33];  // per staged view, rows padded to 33 entries
+  float4 box[kSlots];
+  float4 cam[kSlots][4];
+};
+template <int FMT, bool COUNT, int NW>
+__global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
+    const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi2,
+    const uint32_t* __restrict__ chunks, const uint32_t* __restrict__ nchunks, int stride,
+    const uint32_t* __restrict__ S, const uint32_t* __restrict__ E,
+    const uint32_t* __restrict__ vals, const float4* __restrict__ rec0,
+    const float4* __restrict__ mean4, void* __restrict__ out, unsigned long long* __restrict__ evals,
+    int tsplit) {
+  __shared__ PairStage<NW> s_ws[NW];
+  __shared__ __align__(16) float s_out[kTileSub];
+  __shared__ int s_next;
+  const int W = c_fp.W, H = c_fp.H, TX = c_fp.TX, K = c_fp.K;
+  const long long M = c_fp.M;
+  const int t = c_fp.row0 * TX + (int)(blockIdx.x / (unsigned)tsplit);
+  const int part = (int)(blockIdx.x % (unsigned)tsplit);
+  const int tx = t % TX, ty = t / TX;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PairStage<NW>& ws = s_ws[w];
+  if (threadIdx.x == 0) s_next = 0;
+  const int nch = (int)nchunks[t];
+  const uint32_t* ch_t = chunks + (long long)t * stride;
+  const uint32_t* ps2 = reinterpret_cast<const uint32_t*>(psi2 + (long long)t * kPairSlots);
+  __syncthreads();
+  const float kNaN = __int_as_float(0x7fc00000);
+  unsigned long long nev = 0;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&s_next, 1) * tsplit + part;
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nch) break;
+    const uint32_t ch = ch_t[c];
+    const int start = ch & 1023, nl = ((ch >> 10) & 31) + 1, k = ch >> 16;
+    // this lane's two subpixels, local indices la | lb << 16 (lb = 0xFFFF: a
+    // hole); decoded where needed so that few registers live across the walk
+    const bool mine = lane < nl;
+    const uint32_t pr = mine ? ps2[(start >> 1) + lane] : 0u;
+    auto decode = [&](uint32_t w, int& x, int& y, int& u) {
+      const int l = (int)(w & 0xFFFFu), ly = l / 48, rem = l - 48 * ly;
+      u = rem % 3;
+      x = tx * 16 + rem / 3;
+      y = ty * 16 + ly;
+    };
+    int j = 0;
+    if (mine) {
+      int x, y, u;
+      decode(pr, x, y, u);
+      j = V[((long long)y * W + x) * 3 + u];
+    }
+    const int jlo = __shfl_sync(0xffffffffu, j, 0);
+    const int jhi = __shfl_sync(0xffffffffu, j, nl - 1);
+    const int nsl = jhi - jlo + 1;
+    const int slot = j - jlo;
+    const uint32_t e0 = S[t * K + k], e1 = E[t * K + k];
+    const long long kM = (long long)k * M;
+    for (int g0 = 0; g0 < nsl; g0 += kSlots) {
+      const bool active = mine && slot >= g0 && slot < g0 + kSlots;
+      if (!__any_sync(0xffffffffu, active)) continue;
+      const int ns = min(kSlots, nsl - g0);
+      const int sl = slot - g0;
+      const bool hasb = (pr >> 16) != 0xFFFFu;
+      int xa, ya, ua, xb, yb, ub;
+      decode(pr, xa, ya, ua);
+      if (hasb) decode(pr >> 16, xb, yb, ub); else { xb = xa; yb = ya; ub = ua; }
+      const int bxlo = min(xa, xb), bxhi = max(xa, xb), bylo = min(ya, yb), byhi = max(ya, yb);
+      for (int v = 0; v < ns; ++v) {
+        const bool in = active && sl == v;
+        const int x0 = __reduce_min_sync(0xffffffffu, in ? bxlo : 0x7fffffff);
+        const int x1 = __reduce_max_sync(0xffffffffu, in ? bxhi : -0x7fffffff);
+        const int y0 = __reduce_min_sync(0xffffffffu, in ? bylo : 0x7fffffff);
+        const int y1 = __reduce_max_sync(0xffffffffu, in ? byhi : -0x7fffffff);
+        if (lane == 0)
+          ws.box[v] = make_float4(0.5f * (float)(x0 + x1) + 0.5f, 0.5f * (float)(y0 + y1) + 0.5f,
+                                  0.5f * (float)(x1 - x0), 0.5f * (float)(y1 - y0));
+      }
+      if (lane < 4 * ns)
+        ws.cam[lane >> 2][lane & 3] =
+            reinterpret_cast<const float4*>(&c_cams[jlo + g0 + (lane >> 2)])[lane & 3];
+      __syncwarp();
+      // a saturated (or absent) subpixel gets a NaN position: every later
+      // quadratic form is NaN and fails the blend test, so it never blends again
+      bool da = !active, db = !active || !hasb;
+      f32x2 PX = pk2(da ? kNaN : (float)xa + 0.5f, db ? kNaN : (float)xb + 0.5f);
+      const f32x2 PY = pk2((float)ya + 0.5f, (float)yb + 0.5f);
+      f32x2 T2 = pk2(1.0f, 1.0f), C2 = pk2(0.0f, 0.0f);
+      // batch b's records are gathered at its start, only the next batch's
+      // indices are prefetched: holding the next records in registers (as
+      // k_composite_staged does) costs the occupancy that hides this latency
+      // (measured at C: 10.19 ms with the register prefetch at 48 registers,
+      // 9.67 ms without)
+      uint32_t r_nxt = (e0 + lane < e1) ? vals[e0 + lane] : 0u;
+      for (uint32_t b = e0; b < e1; b += 32) {
+        const Staged cur = gather_entry(rec0, rec0, mean4, r_nxt, b + lane < e1, kM);
+        r_nxt = (b + 32 + lane < e1) ? vals[b + 32 + lane] : 0u;
+        const int slot = 31 - lane;
+        float hx = -1.f, hy = -1.f;
+        if (cur.valid) {
+          ws.rec[slot] = cur.r0;
+          ws.col[slot] = cur.r1;
+          const __half2 ext = *reinterpret_cast<const __half2*>(&cur.r1.w);
+          hx = __low2float(ext);
+          hy = __high2float(ext);
+        }
+        unsigned mymask = 0u;
+        for (int v = 0; v < ns; ++v) {
+          const float2 mu = mean2d_fast4(ws.cam[v][0], ws.cam[v][1], ws.cam[v][2], ws.cam[v][3],
+                                         cur.m.x, cur.m.y, cur.m.z);
+          ws.mu[v * 33 + slot] = mu;
+          const float4 bx = ws.box[v];
+          const bool pass = cur.valid && fabsf(mu.x - bx.x) <= bx.z + hx &&
+                            fabsf(mu.y - bx.y) <= bx.w + hy;
+          const unsigned bits = __ballot_sync(0xffffffffu, pass);
+          if (sl == v) mymask = bits;
+        }
+        __syncwarp();
+        const int n = min(32u, e1 - b);
+        if (!(da && db)) {
+          unsigned mm = __brev(mymask);
+          int qa = -1, qb = -1;
+          const float2* mu_v = &ws.mu[sl * 33];
+          // one base register: entry q's record at rb + 16 q, its colours at
+          // rb + 16 q + 512 + 4 u (u = the subpixel's channel)
+          const uint32_t rb = (uint32_t)__cvta_generic_to_shared(&ws.rec[0]);
+          const uint32_t oa = 512u + 4u * (uint32_t)ua, ob = 512u + 4u * (uint32_t)ub;
+          while (mm) {
+            const int q = msb_pos(mm);
+            mm ^= bit_at(q);
+            const uint32_t ra = rb + 16u * (uint32_t)q;
+            float4 g;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(g.x), "=f"(g.y), "=f"(g.z), "=f"(g.w) : "r"(ra));
+            const float2 m = mu_v[q];
+            const f32x2 dx = sub2(bc2(m.x), PX), dy = sub2(bc2(m.y), PY);
+            const f32x2 q2 = fma2(dx, fma2(bc2(g.x), dx, mul2(bc2(g.y), dy)),
+                                  mul2(mul2(bc2(g.z), dy), dy));
+            const f32x2 t2 = add2(q2, bc2(g.w));
+            const float2 qq = upk2(q2), tt = upk2(t2);
+            const bool oka = tt.x >= kLog2MinAlpha && qq.x <= 0.0f;
+            const bool okb = tt.y >= kLog2MinAlpha && qq.y <= 0.0f;
+            if (oka || okb) {
+              const float aa = oka ? fminf(0.99f, ex2_approx(tt.x)) : 0.0f;
+              const float ab = okb ? fminf(0.99f, ex2_approx(tt.y)) : 0.0f;
+              const f32x2 w2 = mul2(pk2(aa, ab), T2);
+              const f32x2 n2 = sub2(T2, w2);
+              const float2 ww = upk2(w2), tn = upk2(n2), to = upk2(T2);
+              const bool sa = tn.x < 1e-4f, sb = tn.y < 1e-4f;
+              T2 = pk2(sa ? to.x : tn.x, sb ? to.y : tn.y);
+              float ca, cb;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(ca) : "r"(ra + oa));
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(cb) : "r"(ra + ob));
+              C2 = fma2(pk2(ca, cb), pk2(sa ? 0.0f : ww.x, sb ? 0.0f : ww.y), C2);
+              if (sa || sb) {  // a subpixel saturated (Z9): it stops here
+                const float2 px = upk2(PX);
+                PX = pk2(sa ? kNaN : px.x, sb ? kNaN : px.y);
+                if (COUNT) {
+                  if (sa) qa = 31 - q;
+                  if (sb) qb = 31 - q;
+                }
+                da |= sa;
+                db |= sb;
+                if (da && db) mm = 0u;
+              }
+            }
+          }
+          if (COUNT) {
+            if (active) nev += (qa >= 0) ? (unsigned)(qa + 1) : (da ? 0u : (unsigned)n);
+            if (active && hasb) nev += (qb >= 0) ? (unsigned)(qb + 1) : (db ? 0u : (unsigned)n);
+          }
+        }
+        if (__all_sync(0xffffffffu, da && db)) break;
+        __syncwarp();
+      }
+      __syncwarp();
+      if (active) {
+        uint32_t pq;  // re-decode after the walk (nothing of it stays live across)
+        asm volatile("mov.b32 %0, %1;" : "=r"(pq) : "r"(pr));
+        const int la = (int)(pq & 0xFFFFu), lb = (int)(pq >> 16);
+        decode(pq, xa, ya, ua);
+        if (hasb) decode(pq >> 16, xb, yb, ub);
+        const float2 cc = upk2(C2), tt = upk2(T2);
+        const float va = cc.x + c_fp.bg[ua] * tt.x;
+        const float vb = cc.y + c_fp.bg[ub] * tt.y;
+        if (tsplit == 1) {
+          s_out[la] = va;
+          if (hasb) s_out[lb] = vb;
+        } else {
+          const long long oa = ((long long)(ya - c_fp.row0 * 16) * W + xa) * 3 + ua;
+          const long long ob = ((long long)(yb - c_fp.row0 * 16) * W + xb) * 3 + ub;
+          if (FMT == 0) {
+            ((uint8_t*)out)[oa] = (uint8_t)quant_u8(va);
+            if (hasb) ((uint8_t*)out)[ob] = (uint8_t)quant_u8(vb);
+          } else {
+            ((float*)out)[oa] = va;
+            if (hasb) ((float*)out)[ob] = vb;
+          }
         }
       }
     }

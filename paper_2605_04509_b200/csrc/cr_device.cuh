@@ -18,6 +18,7 @@ constexpr int kTile = 16;
 constexpr int kTileSub = kTile * kTile * 3;  // 768 subpixels per tile
 constexpr int kMaxViews = 255;
 constexpr int kMaxCluster = 32;
+constexpr int kPairSlots = 1024;  // paired composite slots per tile (k_pairs_build)
 
 struct __align__(16) CamDev {
   float R[9], t[3], fx, fy, cx, cy;  // 64 B
@@ -89,6 +90,46 @@ __device__ __forceinline__ int clamp_to_int(float v, float lo, float hi) {
   if (v > hi) v = hi;
   return (int)v;
 }
+
+// Packed fp32x2 (sm_100a FADD2 / FMUL2 / FFMA2): each half is the correctly
+// rounded IEEE result of the scalar op (.rn, no FTZ), so packing two
+// independent exact-path operations changes no bit.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(f32x2 r) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+  return f;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// CAUTION: ptxas contracts a packed mul feeding a packed add / sub into one
+// FFMA2 (single rounding) whatever the .rn qualifier or -fmad=false (also
+// fma(a, b, -0) + c), so on the exact path a packed product may only feed a
+// multiply, a compare or a SCALAR add (__fadd_rn is never contracted).
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
 
 struct F3 {
   float x, y, z;
@@ -179,21 +220,31 @@ __device__ __forceinline__ void view_rows(const EllRec& e, float my, int TY, int
 // the row band misses the ellipse.
 __device__ __forceinline__ bool view_row_cols(const EllRec& e, float mx, float my, int ty, int TX,
                                               int& tx0, int& tx1) {
-  const float dlo = xmax(xsub(xadd(xmul(16.0f, (float)ty), 0.5f), my), -e.ey);
-  const float dhi = xmin(xsub(xadd(xmul(16.0f, (float)ty), 15.5f), my), e.ey);
+  // the row's band ends (dlo, dhi) and, below, the slice ends / column
+  // arguments of both sides as packed pairs: the same rounded operations as
+  // the scalar reading of O7, two per instruction
+  const float2 d = upk2(sub2(add2(bc2(xmul(16.0f, (float)ty)), pk2(0.5f, 15.5f)), bc2(my)));
+  const float dlo = xmax(d.x, -e.ey);
+  const float dhi = xmin(d.y, e.ey);
   if (dlo > dhi) return false;
   const float dyR = e.dyR, dyL = -e.dyR;
   const bool rin = dlo <= dyR && dyR <= dhi, lin = dlo <= dyL && dyL <= dhi;
   float right = e.ex, left = -e.ex;
   if (!(rin && lin)) {  // the band misses an x-extreme: evaluate the slice ends
-    const float hlo = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dlo, dlo)))));
-    const float hhi = xsqrt(xmax(0.0f, xmul(e.det, xsub(e.tc, xmul(dhi, dhi)))));
-    const float bl = xmul(e.b, dlo), bh = xmul(e.b, dhi);
-    if (!rin) right = xmax(xmul(xadd(bl, hlo), e.ic), xmul(xadd(bh, hhi), e.ic));
-    if (!lin) left = xmin(xmul(xsub(bl, hlo), e.ic), xmul(xsub(bh, hhi), e.ic));
+    // products packed, the sums after them scalar (see mul2)
+    const f32x2 D = pk2(dlo, dhi);
+    const float2 dd = upk2(mul2(D, D));
+    const float2 hh = upk2(mul2(bc2(e.det), pk2(xsub(e.tc, dd.x), xsub(e.tc, dd.y))));
+    const float hlo = xsqrt(xmax(0.0f, hh.x)), hhi = xsqrt(xmax(0.0f, hh.y));
+    const float2 bb = upk2(mul2(bc2(e.b), D));  // (bl, bh)
+    const float2 r = upk2(mul2(pk2(xadd(bb.x, hlo), xadd(bb.y, hhi)), bc2(e.ic)));
+    const float2 l = upk2(mul2(pk2(xsub(bb.x, hlo), xsub(bb.y, hhi)), bc2(e.ic)));
+    if (!rin) right = xmax(r.x, r.y);
+    if (!lin) left = xmin(l.x, l.y);
   }
-  tx0 = clamp_to_int(ceilf(xmul(xsub(xadd(mx, left), 15.5f), 0.0625f)), 0.0f, (float)TX);
-  tx1 = clamp_to_int(floorf(xmul(xsub(xadd(mx, right), 0.5f), 0.0625f)), -1.0f, (float)(TX - 1));
+  const float2 a = upk2(mul2(sub2(add2(bc2(mx), pk2(left, right)), pk2(15.5f, 0.5f)), bc2(0.0625f)));
+  tx0 = clamp_to_int(ceilf(a.x), 0.0f, (float)TX);
+  tx1 = clamp_to_int(floorf(a.y), -1.0f, (float)(TX - 1));
   return true;
 }
 

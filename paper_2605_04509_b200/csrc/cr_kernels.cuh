@@ -127,6 +127,58 @@ __global__ void k_chunks_build(const uint8_t* __restrict__ V, const uint16_t* __
   nchunks[t] = n;
 }
 
+// Paired work items for the two-subpixels-per-lane composite: per tile, the
+// Psi order with every view run padded to an even length (hole 0xFFFF), so
+// slot pairs (2i, 2i+1) always hold two subpixels of ONE view (or one and a
+// hole); psi2 [T][kPairSlots] u16 (<= 768 subpixels + one hole per run).
+// Each cluster segment is cut into ceil(len/64) equal even-length chunks
+// (greedy: 64-slot chunks and the remainder),
+// packed as start_slot | (lanes-1) << 10 | k << 16 (a lane takes one pair).
+__global__ void k_pairs_build(const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi,
+                              uint16_t* __restrict__ psi2, uint32_t* __restrict__ chunks,
+                              uint32_t* __restrict__ nchunks, int stride, int W, int TX, int TY,
+                              int s, int greedy) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= TX * TY) return;
+  const int tx = t % TX, ty = t / TX;
+  const uint16_t* ps = psi + (long long)t * kTileSub;
+  uint16_t* o2 = psi2 + (long long)t * kPairSlots;
+  uint32_t* out = chunks + (long long)t * stride;
+  int n = 0, nc = 0, cur_j = -1, cur_k = -1, seg = 0, run = 0;
+  auto close_seg = [&](int end) {  // cut [seg, end) into equal even chunks of <= 64 slots
+    const int len = end - seg;
+    if (len <= 0 || cur_k < 0) return;
+    const int np = (len + 63) / 64;
+    const int per = greedy ? 64 : 2 * ((len / 2 + np - 1) / np);  // full warps first, or equal
+    for (int a = seg; a < end; a += per) {
+      const int ln = min(per, end - a);
+      out[nc++] = (uint32_t)a | ((uint32_t)(ln / 2 - 1) << 10) | ((uint32_t)cur_k << 16);
+    }
+  };
+  for (int r = 0; r < kTileSub; ++r) {
+    const int l = ps[r];
+    if (l == 0xFFFF) break;
+    const int ly = l / 48, rem = l % 48, lx = rem / 3, u = rem % 3;
+    const int j = V[((long long)(ty * 16 + ly) * W + tx * 16 + lx) * 3 + u];
+    if (j != cur_j) {
+      if (run & 1) o2[n++] = 0xFFFF;
+      run = 0;
+      const int k = j / s;
+      if (k != cur_k) {
+        close_seg(n);
+        seg = n;
+        cur_k = k;
+      }
+      cur_j = j;
+    }
+    o2[n++] = (uint16_t)l;
+    ++run;
+  }
+  if (run & 1) o2[n++] = 0xFFFF;
+  close_seg(n);
+  nchunks[t] = nc;
+}
+
 // ===========================================================================
 // Upload (O4): Sigma3D = R S S^T R^T in fp64 with explicit rounding (same
 // order as written in DESIGN.md O4), SH transposed to coefficient-major SoA.
@@ -461,6 +513,25 @@ __device__ __forceinline__ bool may_touch_band(int k, int jr, const F3& p, float
 
 // 116 registers, 4 CTAs/SM (measured at config C: capping at 96 / 80
 // registers for 5 / 6 CTAs/SM gives 1.14 / 1.38 ms against 1.13 ms)
+// SH colour (O11) of one Gaussian at two unit view directions (packed halves),
+// the scalar evaluation's operations in the same order per half.
+template <int DEG>
+__device__ __forceinline__ void sh_colour_x2(const float (*sh)[3], f32x2 dx, f32x2 dy, f32x2 dz,
+                                             float2* col) {
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    f32x2 v = mul2(bc2(0.28209479177387814f), bc2(sh[0][ch]));
+    if (DEG >= 1) {
+      // v += -C1 dy s1 + C1 dz s2 - C1 dx s3, as ((a + b) - c) + v, a = -C1 dy s1
+      const f32x2 t1 = mul2(mul2(bc2(-0.4886025119029199f), dy), bc2(sh[1][ch]));
+      const f32x2 t2 = mul2(mul2(bc2(0.4886025119029199f), dz), bc2(sh[2][ch]));
+      const f32x2 t3 = mul2(mul2(bc2(0.4886025119029199f), dx), bc2(sh[3][ch]));
+      v = add2(v, sub2(add2(t1, t2), t3));
+    }
+    col[ch] = upk2(v);
+  }
+}
+
 template <int DEG, bool MB>
 __global__ void __launch_bounds__(128) k_preprocess(
     const float4* __restrict__ mean4, const float4* __restrict__ cov8,
@@ -490,14 +561,9 @@ __global__ void __launch_bounds__(128) k_preprocess(
       for (int q = 0; q < NC; ++q)
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) sh[q][ch] = shsoa[(long long)(q * 3 + ch) * M + i];
-      for (int k = 0; k < K; ++k) {
-        const long long r = (long long)k * M + i;
-        const int jr = c_rep[k];
-        const CamDev& rc = c_cams[jr];
-        const F3 p = cam_point_exact(rc, m.x, m.y, m.z);
-        if (p.z < c_fp.znear) { vis[r] = 0; ++n_near; continue; }
-        float a, b, c, det;
-        if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { vis[r] = 0; ++n_deg; continue; }
+      // the record (i,k) after its exact projection and EWA (a, b, c, det)
+      auto tail = [&](int k, long long r, int jr, const F3& p, float a, float b, float c,
+                      float det) {
         dkey[r] = __float_as_uint(p.z);
         {  // exact per-record AccuTile constants (O7), used by count and emit
           const EllRec el = ell_rec(a, b, c, det, tau);
@@ -505,7 +571,7 @@ __global__ void __launch_bounds__(128) k_preprocess(
                  : !may_touch_band_views(k, m.x, m.y, m.z, el.ex * 1.001f + 1.0f,
                                          el.ey * 1.001f + 1.0f)) {
             vis[r] = 0;  // no view can reach the band / frame: empty union
-            continue;
+            return;
           }
           vis[r] = 1;
           dmn = min(dmn, __float_as_uint(p.z));
@@ -553,6 +619,16 @@ __global__ void __launch_bounds__(128) k_preprocess(
         const float ex = fmaf(sqrtf(tau * a), 1.001f, 0.5f), ey = fmaf(sqrtf(tau * c), 1.001f, 0.5f);
         const __half2 ext = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
         rec0[2 * r + 1] = make_float4(col[0], col[1], col[2], *reinterpret_cast<const float*>(&ext));
+      };
+      for (int k = 0; k < K; ++k) {
+        const long long r = (long long)k * M + i;
+        const int jr = c_rep[k];
+        const CamDev& rc = c_cams[jr];
+        const F3 p = cam_point_exact(rc, m.x, m.y, m.z);
+        if (p.z < c_fp.znear) { vis[r] = 0; ++n_near; continue; }
+        float a, b, c, det;
+        if (!cov2d_exact(rc, c_ccon[jr], p, S6, a, b, c, det)) { vis[r] = 0; ++n_deg; continue; }
+        tail(k, r, jr, p, a, b, c, det);
       }
     }
   }

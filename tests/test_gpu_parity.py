@@ -488,3 +488,31 @@ def test_async_host_output(cfgA_pair):
     for h, r_ in zip(hosts, ref):
         assert np.array_equal(h.numpy(), r_)
     g.set_camera_rig(c.make_rig())
+
+
+@pytest.mark.parametrize("name,s,rows", [("A", 8, None), ("A", 1, None), ("A", 3, (2, 5)),
+                                         ("B", 8, (60, 64)), ("P4K", 18, (40, 43))])
+def test_pairs_composite_equals_one_subpixel_per_lane(monkeypatch, name, s, rows):
+    # k_composite_pairs (two subpixels of one view per lane, packed fp32x2 blend,
+    # view runs padded to even length) against k_composite_staged (CR_EXP bit 6):
+    # same per-subpixel operations in the same order, so frames (float and RGB8)
+    # and evaluation counts must be identical; rows exercise the tile split path
+    _need_gpu()
+    from paper_2605_04509_b200 import CoherentRaster
+    c = sy.CONFIGS[name]
+    scene = c.make_scene()
+    out = {}
+    for exp in ("0", "64"):
+        monkeypatch.setenv("CR_EXP", exp)
+        g = CoherentRaster(0)
+        g.upload_gaussians(scene)
+        g.set_display(c.W, c.H, c.N, c.lens_pitch, c.slant, c.center_offset)
+        g.set_camera_rig(c.make_rig())
+        f = g.render(s, output_format="float", rows=rows, background=(0.1, 0.2, 0.3)).cpu().numpy()
+        b = g.render(s, output_format="rgb8", rows=rows).cpu().numpy()
+        g.render(s, rows=rows, stats=True, count_evals=True)
+        out[exp] = (f, b, g.last_stats["evals"])
+        g.close()
+    assert np.array_equal(out["0"][0], out["64"][0])
+    assert np.array_equal(out["0"][1], out["64"][1])
+    assert out["0"][2] == out["64"][2]

@@ -53,7 +53,7 @@ def main():
                P2_it=0, P2_stage=0, P2_stage_views=0, sub=0, evals=0, visits_ideal=0,
                A_nosat_it=0, visits_nosat=0, V1_it=0, V1_stage=0, A_union_it=0,
                Ay2_it=0, Ay2_masks=0, Aq4_it=0, Aq4_masks=0, H2_it=0, H2_masks=0, H2_stage=0,
-               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0, R_it=0, R_stage=0, R_stage_views=0)
+               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0, R_it=0, R_stage=0, R_stage_views=0, P2v_it=0, P2v_stage=0, P2v_stage_views=0, P2v_pairs=0, contrib_visits=0)
     for t in tiles:
         tx, ty = t % TX, t // TX
         ls = psi[t]
@@ -221,6 +221,28 @@ def main():
                                for ln in lanes])
                 for b in range(nb):
                     tot["P2_it"] += int(lm[:, b * 32:(b + 1) * 32].sum(1).max())
+
+            # ---- P2v: same-view pairs (each view run padded to an even length),
+            # chunks of <= 32 pairs inside the cluster segment
+            pairs = []
+            for jj in np.unique(js):
+                m = np.nonzero(js == jj)[0]
+                for q in range(0, m.size, 2):
+                    pairs.append(m[q:q + 2])
+            tot["P2v_pairs"] += len(pairs)
+            for c0 in range(0, len(pairs), 32):
+                lanes = pairs[c0:c0 + 32]
+                mem = np.concatenate(lanes)
+                bx = boxes(mem)
+                last = int(stop[mem].max())
+                nb = (last + 31) // 32
+                tot["P2v_stage"] += nb
+                tot["P2v_stage_views"] += nb * len(bx)
+                lm = np.stack([bx[js[ln[0]]] & (idx < stop[ln].max()) for ln in lanes])
+                for b in range(nb):
+                    tot["P2v_it"] += int(lm[:, b * 32:(b + 1) * 32].sum(1).max())
+            for q in range(nsub):
+                tot["contrib_visits"] += int((contrib[q] & (idx < stop[q])).sum())
     print(name, "tiles", len(tiles), tot)
     A = tot["A_it"]
     print(f"visits(ideal lane work)/32 = {tot['visits_ideal']/32:.0f}  A iterations {A}  "
@@ -238,3 +260,4 @@ def main():
 
 if __name__ == "__main__":
     main()
+
