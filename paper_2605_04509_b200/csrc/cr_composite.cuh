@@ -382,7 +382,7 @@ __device__ __forceinline__ unsigned bit_at(int q) {  // 1u << q in one BMSK
 }
 
 #ifndef CR_COMP2_MINB
-#define CR_COMP2_MINB 10  // 48 registers: 10 CTAs x 4 warps per SM (measured: 11 -> 40 regs spills)
+#define CR_COMP2_MINB 10  // 48 registers, 10 CTAs x 4 warps per SM (measured at C: 9 -> 8.63 ms, 10 -> 8.36, 11 -> 10.9)
 #endif
 template <int NW>
 struct PairStage {  // one warp's staging area (rec / col share the entry offset 16 q)
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
         if (!(da && db)) {
           unsigned mm = __brev(mymask);
           int qa = -1, qb = -1;
-          const float2* mu_v = &ws.mu[sl * 33];
+          const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&ws.mu[sl * 33]);
           // one base register: entry q's record at rb + 16 q, its colours at
           // rb + 16 q + 512 + 4 u (u = the subpixel's channel)
           const uint32_t rb = (uint32_t)__cvta_generic_to_shared(&ws.rec[0]);
@@ -522,7 +522,8 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
             float4 g;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(g.x), "=f"(g.y), "=f"(g.z), "=f"(g.w) : "r"(ra));
-            const float2 m = mu_v[q];
+            float2 m;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(m.x), "=f"(m.y) : "r"(mb + 8u * (uint32_t)q));
             const f32x2 dx = sub2(bc2(m.x), PX), dy = sub2(bc2(m.y), PY);
             const f32x2 q2 = fma2(dx, fma2(bc2(g.x), dx, mul2(bc2(g.y), dy)),
                                   mul2(mul2(bc2(g.z), dy), dy));

@@ -53,7 +53,7 @@ def main():
                P2_it=0, P2_stage=0, P2_stage_views=0, sub=0, evals=0, visits_ideal=0,
                A_nosat_it=0, visits_nosat=0, V1_it=0, V1_stage=0, A_union_it=0,
                Ay2_it=0, Ay2_masks=0, Aq4_it=0, Aq4_masks=0, H2_it=0, H2_masks=0, H2_stage=0,
-               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0, R_it=0, R_stage=0, R_stage_views=0, P2v_it=0, P2v_stage=0, P2v_stage_views=0, P2v_pairs=0, contrib_visits=0)
+               H2q_it=0, H2q_masks=0, As_it=0, As_masks=0, R_it=0, R_stage=0, R_stage_views=0, P2v_it=0, P2v_stage=0, P2v_stage_views=0, P2v_pairs=0, contrib_visits=0, P2g_it=0, P2g_stage=0, P2g_stage_views=0, P4v_it=0, P4v_stage=0, P4v_stage_views=0)
     for t in tiles:
         tx, ty = t % TX, t // TX
         ls = psi[t]
@@ -243,6 +243,25 @@ def main():
                     tot["P2v_it"] += int(lm[:, b * 32:(b + 1) * 32].sum(1).max())
             for q in range(nsub):
                 tot["contrib_visits"] += int((contrib[q] & (idx < stop[q])).sum())
+            # ---- P2g: P2v lanes, chunks of 32 lanes then the remainder (greedy);
+            # P4v: four same-view subpixels per lane (view runs padded to 4)
+            for key, per in (("P2g", 2), ("P4v", 4)):
+                groups = []
+                for jj in np.unique(js):
+                    m = np.nonzero(js == jj)[0]
+                    for q in range(0, m.size, per):
+                        groups.append(m[q:q + per])
+                for c0 in range(0, len(groups), 32):
+                    lanes = groups[c0:c0 + 32]
+                    mem = np.concatenate(lanes)
+                    bx = boxes(mem)
+                    last = int(stop[mem].max())
+                    nb = (last + 31) // 32
+                    tot[key + "_stage"] += nb
+                    tot[key + "_stage_views"] += nb * len(bx)
+                    lm = np.stack([bx[js[ln[0]]] & (idx < stop[ln].max()) for ln in lanes])
+                    for b in range(nb):
+                        tot[key + "_it"] += int(lm[:, b * 32:(b + 1) * 32].sum(1).max())
     print(name, "tiles", len(tiles), tot)
     A = tot["A_it"]
     print(f"visits(ideal lane work)/32 = {tot['visits_ideal']/32:.0f}  A iterations {A}  "
