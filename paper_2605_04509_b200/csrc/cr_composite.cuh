@@ -384,6 +384,18 @@ __device__ __forceinline__ unsigned bit_at(int q) {  // 1u << q in one BMSK
 #ifndef CR_COMP2_MINB
 #define CR_COMP2_MINB 10  // 48 registers, 10 CTAs x 4 warps per SM (measured at C: 9 -> 8.63 ms, 10 -> 8.36, 11 -> 10.9)
 #endif
+// mean2d_fast4 with its last multiply / fma on the (x, y) pair packed
+// (same operations per half: bit-identical)
+__device__ __forceinline__ float2 mean2d_fast4x(const float4 a, const float4 b, const float4 c,
+                                                const float4 d, float mx, float my, float mz) {
+  const float px = fmaf(a.x, mx, fmaf(a.y, my, fmaf(a.z, mz, c.y)));
+  const float py = fmaf(a.w, mx, fmaf(b.x, my, fmaf(b.y, mz, c.z)));
+  const float pz = fmaf(b.z, mx, fmaf(b.w, my, fmaf(c.x, mz, c.w)));
+  if (!(pz >= c_fp.znear)) return make_float2(1e18f, 1e18f);
+  const float iz = rcp_approx(pz);
+  return upk2(fma2(pk2(d.x, d.y), mul2(pk2(px, py), bc2(iz)), pk2(d.z, d.w)));
+}
+
 template <int NW>
 struct PairStage {  // one warp's staging area (rec / col share the entry offset 16 q)
   float4 rec[32];
@@ -496,12 +508,13 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
         }
         unsigned mymask = 0u;
         for (int v = 0; v < ns; ++v) {
-          const float2 mu = mean2d_fast4(ws.cam[v][0], ws.cam[v][1], ws.cam[v][2], ws.cam[v][3],
-                                         cur.m.x, cur.m.y, cur.m.z);
+          const float2 mu = mean2d_fast4x(ws.cam[v][0], ws.cam[v][1], ws.cam[v][2], ws.cam[v][3],
+                                          cur.m.x, cur.m.y, cur.m.z);
           ws.mu[v * 33 + slot] = mu;
           const float4 bx = ws.box[v];
-          const bool pass = cur.valid && fabsf(mu.x - bx.x) <= bx.z + hx &&
-                            fabsf(mu.y - bx.y) <= bx.w + hy;
+          const float2 dd = upk2(sub2(pk2(mu.x, mu.y), pk2(bx.x, bx.y)));
+          const float2 lim = upk2(add2(pk2(bx.z, bx.w), pk2(hx, hy)));
+          const bool pass = cur.valid && fabsf(dd.x) <= lim.x && fabsf(dd.y) <= lim.y;
           const unsigned bits = __ballot_sync(0xffffffffu, pass);
           if (sl == v) mymask = bits;
         }
