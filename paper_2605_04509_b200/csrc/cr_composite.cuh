@@ -384,16 +384,25 @@ __device__ __forceinline__ unsigned bit_at(int q) {  // 1u << q in one BMSK
 #ifndef CR_COMP2_MINB
 #define CR_COMP2_MINB 10  // 48 registers, 10 CTAs x 4 warps per SM (measured at C: 9 -> 8.63 ms, 10 -> 8.36, 11 -> 10.9)
 #endif
-// mean2d_fast4 with its last multiply / fma on the (x, y) pair packed
-// (same operations per half: bit-identical)
-__device__ __forceinline__ float2 mean2d_fast4x(const float4 a, const float4 b, const float4 c,
-                                                const float4 d, float mx, float my, float mz) {
-  const float px = fmaf(a.x, mx, fmaf(a.y, my, fmaf(a.z, mz, c.y)));
-  const float py = fmaf(a.w, mx, fmaf(b.x, my, fmaf(b.y, mz, c.z)));
-  const float pz = fmaf(b.z, mx, fmaf(b.w, my, fmaf(c.x, mz, c.w)));
+// mean2d_fast4 with the (x, y) rows packed: the camera staged as
+// q0 = (R0, R3, R1, R4), q1 = (R2, R5, t0, t1), q2 = (R6, R7, R8, t2),
+// q3 = (fx, fy, cx, cy), so each (x, y) operand pair is one register pair
+// (same operations per half as mean2d_fast4: bit-identical)
+__device__ __forceinline__ void cam_pairs(const CamDev& c, float4* q) {
+  q[0] = make_float4(c.R[0], c.R[3], c.R[1], c.R[4]);
+  q[1] = make_float4(c.R[2], c.R[5], c.t[0], c.t[1]);
+  q[2] = make_float4(c.R[6], c.R[7], c.R[8], c.t[2]);
+  q[3] = make_float4(c.fx, c.fy, c.cx, c.cy);
+}
+__device__ __forceinline__ float2 mean2d_fast_pairs(const float4 q0, const float4 q1,
+                                                    const float4 q2, const float4 q3, float mx,
+                                                    float my, float mz) {
+  const f32x2 pxy = fma2(pk2(q0.x, q0.y), bc2(mx),
+                         fma2(pk2(q0.z, q0.w), bc2(my), fma2(pk2(q1.x, q1.y), bc2(mz), pk2(q1.z, q1.w))));
+  const float pz = fmaf(q2.x, mx, fmaf(q2.y, my, fmaf(q2.z, mz, q2.w)));
   if (!(pz >= c_fp.znear)) return make_float2(1e18f, 1e18f);
   const float iz = rcp_approx(pz);
-  return upk2(fma2(pk2(d.x, d.y), mul2(pk2(px, py), bc2(iz)), pk2(d.z, d.w)));
+  return upk2(fma2(pk2(q3.x, q3.y), mul2(pxy, bc2(iz)), pk2(q3.z, q3.w)));
 }
 
 template <int NW>
@@ -478,9 +487,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
           ws.box[v] = make_float4(0.5f * (float)(x0 + x1) + 0.5f, 0.5f * (float)(y0 + y1) + 0.5f,
                                   0.5f * (float)(x1 - x0), 0.5f * (float)(y1 - y0));
       }
-      if (lane < 4 * ns)
-        ws.cam[lane >> 2][lane & 3] =
-            reinterpret_cast<const float4*>(&c_cams[jlo + g0 + (lane >> 2)])[lane & 3];
+      if (lane < ns) cam_pairs(c_cams[jlo + g0 + lane], ws.cam[lane]);
       __syncwarp();
       // a saturated (or absent) subpixel gets a NaN position: every later
       // quadratic form is NaN and fails the blend test, so it never blends again
@@ -508,8 +515,8 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
         }
         unsigned mymask = 0u;
         for (int v = 0; v < ns; ++v) {
-          const float2 mu = mean2d_fast4x(ws.cam[v][0], ws.cam[v][1], ws.cam[v][2], ws.cam[v][3],
-                                          cur.m.x, cur.m.y, cur.m.z);
+          const float2 mu = mean2d_fast_pairs(ws.cam[v][0], ws.cam[v][1], ws.cam[v][2],
+                                              ws.cam[v][3], cur.m.x, cur.m.y, cur.m.z);
           ws.mu[v * 33 + slot] = mu;
           const float4 bx = ws.box[v];
           const float2 dd = upk2(sub2(pk2(mu.x, mu.y), pk2(bx.x, bx.y)));
