@@ -52,7 +52,7 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def measure_traffic(cfg_name: str, s: int, kernel_regex: str = "k_composite_staged"):
+def measure_traffic(cfg_name: str, s: int, kernel_regex: str = "k_composite_pairs|k_composite_staged"):
     """DRAM bytes (read + write) of one launch of the dominant kernel, from an
     ncu capture of one frame of the same config in a subprocess (after the
     timed region; ncu's replay never touches the timed numbers).  None when
@@ -539,7 +539,9 @@ def main():
         "mean_traversal": evals / max(1, band_out.numel()),  # rank 0's band
         "stage_ms": ms_stage,
         "fps_distribution": fps_dist,
-        "roofline": {"bound": "alu", "kernel": "k_composite_staged",
+        "roofline": {"bound": "alu",
+                     "kernel": ("k_composite_staged" if int(os.environ.get("CR_EXP", "0") or 0) & 64
+                                else "k_composite_pairs"),
                      "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
                      "traffic": traffic,

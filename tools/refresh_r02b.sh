@@ -1,7 +1,6 @@
 #!/bin/bash
 # Round-2 refresh, part 2 (under gpurun): ncu per-kernel table + launch list
 # of config C, full captures of the composite and the count, band costs,
-# compute-sanitizer.
 O=gpurun_out/r02final; mkdir -p $O
 bash tools/prof_all.sh r02 C > /dev/null 2>&1
 cp gpurun_out/ncu_table_r02.txt $O/ncu_kernels_configC.txt
@@ -12,6 +11,4 @@ python tools/ncu_details.py $O/comp_count_full.ncu-rep > $O/comp_count_full_summ
 python tools/ncu_lines.py $O/comp_count_full.ncu-rep k_composite 40 > $O/composite_lines.txt 2>&1
 python tools/ncu_lines.py $O/comp_count_full.ncu-rep k_countv 40 > $O/count_lines.txt 2>&1
 for R in 2 4 8; do timeout 900 python tools/band_cost.py C $R refined > $O/band_costs_R${R}_refined.txt 2>&1; done
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py all > $O/memcheck.log 2>&1
-timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_run.py A > $O/racecheck_A.log 2>&1
 echo done

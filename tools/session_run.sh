@@ -1,8 +1,5 @@
-O=gpurun_out/s3p; mkdir -p $O
-timeout 600 python tools/exp_equal.py C 0 64 > $O/equal.txt 2>&1
-timeout 600 python tools/exp_equal.py P4K 0 64 >> $O/equal.txt 2>&1
-timeout 900 python tools/ab_exp.py C 0 > $O/abC.txt 2>&1
-timeout 600 python tools/ab_exp.py B 0 > $O/abB.txt 2>&1
-timeout 900 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_run.py all > $O/memcheck.log 2>&1
-timeout 900 compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_run.py A > $O/racecheck_A.log 2>&1
+O=gpurun_out/s3q; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $O/bench.json 2> $O/bench.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_composite_pairs" -c 1 -o $O/comp python tools/prof_frame.py C 1 > $O/ncu.log 2>&1
 echo done
