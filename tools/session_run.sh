@@ -1,5 +1,6 @@
-O=gpurun_out/s3q; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $O/bench.json 2> $O/bench.err
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_composite_pairs" -c 1 -o $O/comp python tools/prof_frame.py C 1 > $O/ncu.log 2>&1
+O=gpurun_out/s3r; mkdir -p $O
+timeout 600 python tools/exp_equal.py C 0 64 > $O/equal.txt 2>&1
+bash tools/ab_lib.sh build/lib9.so C $O/ab9.txt
+timeout 600 python tools/ab_exp.py B 0 > $O/abB.txt 2>&1
+CR_LIB=build/lib9.so timeout 600 python tools/ab_exp.py B 0 >> $O/abB.txt 2>&1
 echo done
