@@ -83,6 +83,9 @@ __device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b)
 __device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float xdiv(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float xsqrt(float a) { return __fsqrt_rn(a); }
+// sqrt of a value already clamped to >= +0: +0 skips __fsqrt_rn, whose range
+// check sends zero to its slow-path subroutine (same result, +0)
+__device__ __forceinline__ float xsqrt_nn(float a) { return a > 0.0f ? __fsqrt_rn(a) : a; }
 __device__ __forceinline__ float xmin(float a, float b) { return (b < a) ? b : a; }
 __device__ __forceinline__ float xmax(float a, float b) { return (a < b) ? b : a; }
 __device__ __forceinline__ int clamp_to_int(float v, float lo, float hi) {
@@ -235,7 +238,7 @@ __device__ __forceinline__ bool view_row_cols(const EllRec& e, float mx, float m
     const f32x2 D = pk2(dlo, dhi);
     const float2 dd = upk2(mul2(D, D));
     const float2 hh = upk2(mul2(bc2(e.det), pk2(xsub(e.tc, dd.x), xsub(e.tc, dd.y))));
-    const float hlo = xsqrt(xmax(0.0f, hh.x)), hhi = xsqrt(xmax(0.0f, hh.y));
+    const float hlo = xsqrt_nn(xmax(0.0f, hh.x)), hhi = xsqrt_nn(xmax(0.0f, hh.y));
     const float2 bb = upk2(mul2(bc2(e.b), D));  // (bl, bh)
     const float2 r = upk2(mul2(pk2(xadd(bb.x, hlo), xadd(bb.y, hhi)), bc2(e.ic)));
     const float2 l = upk2(mul2(pk2(xsub(bb.x, hlo), xsub(bb.y, hhi)), bc2(e.ic)));
