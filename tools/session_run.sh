@@ -1,6 +1,6 @@
-O=gpurun_out/s3s; mkdir -p $O
-./tools/x2check/vrc_check > $O/vrc.txt 2>&1
-bash tools/ab_lib.sh build/libhead.so C $O/ab_sqrt.txt
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -q -x > $O/pytest.log 2>&1
-bash tools/refresh_r02b.sh
+O=gpurun_out/s3t; mkdir -p $O
+timeout 600 python tools/exp_equal.py C 0 4096 > $O/equal.txt 2>&1
+timeout 900 python tools/ab_exp.py C 0,4096 > $O/abC.txt 2>&1
+timeout 600 python tools/ab_exp.py B 0,4096 > $O/abB.txt 2>&1
+timeout 900 python bench.py > $O/bench_configC.json 2> $O/bench_configC.err
 echo done
