@@ -1169,9 +1169,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
       P_<float4>(c->rec0), P_<float4>(c->rec0) + 1, m4, dst, evals, tsplit)
 #define CR_PAIRS(F, CNT)                                                                      \
-  if (c->exp & 4096) CR_PAIRS1(F, CNT, 2); else CR_PAIRS1(F, CNT, kCompWarps)
-#define CR_PAIRS1(F, CNT, NWV)                                                                \
-  k_composite_pairs<F, CNT, NWV><<<ntile * tsplit, NWV * 32, 0, str>>>(                       \
+  k_composite_pairs<F, CNT, kCompWarps><<<ntile * tsplit, kCompWarps * 32, 0, str>>>(          \
       P_<uint8_t>(c->V), P_<uint16_t>(c->psi2), P_<uint32_t>(c->chunks),                      \
       P_<uint32_t>(c->nchunks), c->chunk_stride, P_<uint32_t>(c->S), P_<uint32_t>(c->E), pA, \
       P_<float4>(c->rec0), m4, dst, evals, tsplit)
@@ -1212,7 +1210,6 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   }
 #undef CR_STAGED
 #undef CR_PAIRS
-#undef CR_PAIRS1
 #undef CR_STAGED1
 #undef CR_THREAD
   CR_LAUNCHED(c);

@@ -414,7 +414,7 @@ struct PairStage {  // one warp's staging area (rec / col share the entry offset
   float4 cam[kSlots][4];
 };
 template <int FMT, bool COUNT, int NW>
-__global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB * 4 / NW) k_composite_pairs(
+__global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
     const uint8_t* __restrict__ V, const uint16_t* __restrict__ psi2,
     const uint32_t* __restrict__ chunks, const uint32_t* __restrict__ nchunks, int stride,
     const uint32_t* __restrict__ S, const uint32_t* __restrict__ E,
