@@ -491,8 +491,10 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
       __syncwarp();
       // a saturated (or absent) subpixel gets a NaN position: every later
       // quadratic form is NaN and fails the blend test, so it never blends again
-      bool da = !active, db = !active || !hasb;
-      f32x2 PX = pk2(da ? kNaN : (float)xa + 0.5f, db ? kNaN : (float)xb + 0.5f);
+      // done flags: bit 0 subpixel a, bit 1 subpixel b (saturated or absent)
+      uint32_t dd = (active ? 0u : 3u) | (hasb ? 0u : 2u);
+      const bool da0 = (dd & 1u) != 0u, db0 = (dd & 2u) != 0u;
+      f32x2 PX = pk2(da0 ? kNaN : (float)xa + 0.5f, db0 ? kNaN : (float)xb + 0.5f);
       const f32x2 PY = pk2((float)ya + 0.5f, (float)yb + 0.5f);
       f32x2 T2 = pk2(1.0f, 1.0f), C2 = pk2(0.0f, 0.0f);
       // batch b's records are gathered at its start, only the next batch's
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
         }
         __syncwarp();
         const int n = min(32u, e1 - b);
-        if (!(da && db)) {
+        if (dd != 3u) {
           unsigned mm = __brev(mymask);
           int qa = -1, qb = -1;
           const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&ws.mu[sl * 33]);
@@ -570,18 +572,17 @@ __global__ void __launch_bounds__(NW * 32, CR_COMP2_MINB) k_composite_pairs(
                   if (sa) qa = 31 - q;
                   if (sb) qb = 31 - q;
                 }
-                da |= sa;
-                db |= sb;
-                if (da && db) mm = 0u;
+                dd |= (sa ? 1u : 0u) | (sb ? 2u : 0u);
+                if (dd == 3u) mm = 0u;
               }
             }
           }
           if (COUNT) {
-            if (active) nev += (qa >= 0) ? (unsigned)(qa + 1) : (da ? 0u : (unsigned)n);
-            if (active && hasb) nev += (qb >= 0) ? (unsigned)(qb + 1) : (db ? 0u : (unsigned)n);
+            if (active) nev += (qa >= 0) ? (unsigned)(qa + 1) : ((dd & 1u) ? 0u : (unsigned)n);
+            if (active && hasb) nev += (qb >= 0) ? (unsigned)(qb + 1) : ((dd & 2u) ? 0u : (unsigned)n);
           }
         }
-        if (__all_sync(0xffffffffu, da && db)) break;
+        if (__all_sync(0xffffffffu, dd == 3u)) break;
         __syncwarp();
       }
       __syncwarp();
