@@ -176,6 +176,17 @@ __global__ void k_pairs_build(const uint8_t* __restrict__ V, const uint16_t* __r
   }
   if (run & 1) o2[n++] = 0xFFFF;
   close_seg(n);
+  if (greedy & 2) {  // full 32-lane chunks first, the short remainders last (they fill the
+                     // tile's tail while the last full chunks finish)
+    uint32_t tmp[kMaxViews + 24];  // local: this kernel runs once per display and s
+    for (int q = 0; q < nc; ++q) tmp[q] = out[q];
+    int w = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int q = 0; q < nc; ++q) {
+        const bool full = ((tmp[q] >> 10) & 31u) == 31u;
+        if (full == (pass == 0)) out[w++] = tmp[q];
+      }
+  }
   nchunks[t] = nc;
 }
 
@@ -289,6 +300,13 @@ __device__ __forceinline__ unsigned long long gor64(unsigned long long v) {
 #pragma unroll
   for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// len set bits from bit pos (pos < 32, len >= 1; bits past 31 dropped): one BMSK
+__device__ __forceinline__ unsigned bmsk32(int pos, int len) {
+  unsigned r;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(r) : "r"(pos), "r"(len));
+  return r;
 }
 
 // Position of the n-th (0-based) set bit of x (n < popc(x)): popcount
@@ -806,12 +824,13 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
           if (tx0 < slo || tx1 - slo >= 64) {
             atomicOr(&s_flag[w][gs], 1);
           } else {
-            const int len = tx1 - tx0 + 1;
-            const unsigned long long bits =
-                ((len >= 64) ? ~0ull : ((1ull << len) - 1ull)) << (tx0 - slo);
+            // bits [a, b] of the 64-column window as two 32-bit words (BMSK)
+            const int a = tx0 - slo, b = tx1 - slo;
+            const unsigned lo = bmsk32(a, b - a + 1);
+            const unsigned hi = b >= 32 ? bmsk32(max(a - 32, 0), b - max(a, 32) + 1) : 0u;
             unsigned* mw = reinterpret_cast<unsigned*>(&s_mask[w][gs][row - srmin]);
-            if ((unsigned)bits) atomicOr(mw, (unsigned)bits);
-            if ((unsigned)(bits >> 32)) atomicOr(mw + 1, (unsigned)(bits >> 32));
+            if (lo) atomicOr(mw, lo);
+            if (hi) atomicOr(mw + 1, hi);
           }
         }
       }
