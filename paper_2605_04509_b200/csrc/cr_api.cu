@@ -909,8 +909,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       CR_TRY(ensure(c, c->psi2, (size_t)TX * TY * kPairSlots * 2));
       k_pairs_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
           P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint16_t>(c->psi2), P_<uint32_t>(c->chunks),
-          P_<uint32_t>(c->nchunks), stride, W, TX, TY, s,
-          ((c->exp & 2048) ? 0 : 1) | ((c->exp & 4096) ? 2 : 0));
+          P_<uint32_t>(c->nchunks), stride, W, TX, TY, s, (c->exp & 2048) ? 0 : 1);
     } else {
       k_chunks_build<<<grid_for((long long)TX * TY, 128), 128, 0, str>>>(
           P_<uint8_t>(c->V), P_<uint16_t>(c->psi), P_<uint32_t>(c->chunks),

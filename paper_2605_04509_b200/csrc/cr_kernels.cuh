@@ -176,17 +176,6 @@ __global__ void k_pairs_build(const uint8_t* __restrict__ V, const uint16_t* __r
   }
   if (run & 1) o2[n++] = 0xFFFF;
   close_seg(n);
-  if (greedy & 2) {  // full 32-lane chunks first, the short remainders last (they fill the
-                     // tile's tail while the last full chunks finish)
-    uint32_t tmp[kMaxViews + 24];  // local: this kernel runs once per display and s
-    for (int q = 0; q < nc; ++q) tmp[q] = out[q];
-    int w = 0;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int q = 0; q < nc; ++q) {
-        const bool full = ((tmp[q] >> 10) & 31u) == 31u;
-        if (full == (pass == 0)) out[w++] = tmp[q];
-      }
-  }
   nchunks[t] = nc;
 }
 
