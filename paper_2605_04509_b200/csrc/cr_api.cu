@@ -1026,20 +1026,20 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     // than 64-record blocks of work
     const unsigned count_grid =
         (unsigned)std::min<long long>(148 * 64, std::max<long long>(148, ((long long)nvis + 63) / 64));
+#define CR_COUNTL(GL, VL)                                                                      \
+  k_countv<GL, VL><<<count_grid, kBinThreads, cam_smem, str>>>(                                 \
+      rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),        \
+      P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6)
+  // lanes per record x views per lane (measured at C, s = 8: 4 x 2 -> 2 x 4 lanes/views
+  // took binning 5.65 -> 5.28 ms, s = 4: 4 x 1 -> 2 x 2 7.29 -> 6.21 ms; P2K s = 16:
+  // 4 x 4 no faster than 8 x 2; P4K s = 18: 8 x 3 instead of 16 x 2, 9.2 -> 8.3 ms)
 #define CR_COUNTS(GG)                                                                         \
-  if (GG == 32 && s <= 24) /* 17..24 views: three per lane, 8-lane groups (P4K s=18:      \
-                                binning 9.2 -> 8.3 ms vs 16 lanes x 2 views) */              \
-    k_countv<8, 3><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
-        rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
-  else if (GG >= 8) /* two views per lane */                                                  \
-    k_countv<(GG >= 8 ? GG / 2 : 1), 2><<<count_grid, kBinThreads, cam_smem, str>>>(          \
-        rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
-  else                                                                                        \
-    k_countv<GG, 1><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
-        rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
+  if (GG == 32 && s <= 24) CR_COUNTL(8, 3);                                                   \
+  else if (GG == 8) CR_COUNTL(2, 4);                                                          \
+  else if (GG == 4) CR_COUNTL(2, 2);                                                          \
+  else if (GG == 2 && (c->exp & 4096)) CR_COUNTL(1, 2);                                       \
+  else if (GG >= 8) CR_COUNTL((GG >= 8 ? GG / 2 : 1), 2);                                     \
+  else CR_COUNTL(GG, 1);                                                                      \
   CR_LAUNCHED(c);                                                                             \
   k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                   \
       P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
@@ -1053,6 +1053,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       default: CR_COUNTS(32); break;
     }
 #undef CR_COUNTS
+#undef CR_COUNTL
     CR_LAUNCHED(c);
     CR_TRACE(c, "count");
     CR_TRY(dev_scan(c, Scan::InArr{P_<uint32_t>(c->cnt)}, Scan::OutStore{P_<uint32_t>(c->offs)},
