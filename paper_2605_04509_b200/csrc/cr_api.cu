@@ -1031,13 +1031,14 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),        \
       P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6)
   // lanes per record x views per lane (measured at C, s = 8: 4 x 2 -> 2 x 4 lanes/views
-  // took binning 5.65 -> 5.28 ms, s = 4: 4 x 1 -> 2 x 2 7.29 -> 6.21 ms; P2K s = 16:
+  // took binning 5.65 -> 5.28 ms, s = 4: 4 x 1 -> 2 x 2 7.29 -> 6.21 ms, s = 2: 2 x 1 ->
+  // 1 x 2 9.46 -> 8.70 ms; P2K s = 16:
   // 4 x 4 no faster than 8 x 2; P4K s = 18: 8 x 3 instead of 16 x 2, 9.2 -> 8.3 ms)
 #define CR_COUNTS(GG)                                                                         \
   if (GG == 32 && s <= 24) CR_COUNTL(8, 3);                                                   \
   else if (GG == 8) CR_COUNTL(2, 4);                                                          \
   else if (GG == 4) CR_COUNTL(2, 2);                                                          \
-  else if (GG == 2 && (c->exp & 4096)) CR_COUNTL(1, 2);                                       \
+  else if (GG == 2) CR_COUNTL(1, 2);                                                          \
   else if (GG >= 8) CR_COUNTL((GG >= 8 ? GG / 2 : 1), 2);                                     \
   else CR_COUNTL(GG, 1);                                                                      \
   CR_LAUNCHED(c);                                                                             \
