@@ -680,8 +680,8 @@ constexpr int kBinWarps = kBinThreads / 32;
 // records per step, halving the per-record share of loads, group reductions,
 // the item prefix scan and the slot write (measured: binning 7.56 -> 6.58 ms
 // at config C; VPL = 4: 6.54 ms, not worth its 77 registers).
-template <int G, int VPL>
-__global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restrict__ recs,
+template <int G, int VPL, int NTH = kBinThreads>
+__global__ void __launch_bounds__(NTH) k_countv(const uint32_t* __restrict__ recs,
                                                         uint32_t n,
                                                         const float4* __restrict__ mean4,
                                                         const float4* __restrict__ geom,
@@ -689,21 +689,22 @@ __global__ void __launch_bounds__(kBinThreads) k_countv(const uint32_t* __restri
                                                         uint4* __restrict__ slots,
                                                         uint32_t* __restrict__ big,
                                                         uint32_t* __restrict__ n_big) {
+  constexpr int kBW = NTH / 32;  // warps per block
   extern __shared__ float s_cam[];  // c_fp.N cameras x kCamStride (dynamic)
-  __shared__ unsigned long long s_mask[kBinWarps][32][kSlotRows];  // [warp][group][row]
-  __shared__ int s_flag[kBinWarps][32];
-  __shared__ int s_src[kBinWarps][32];
-  __shared__ int s_seg[kBinWarps][32];            // per lane: first item of its segment
-  __shared__ float4 s_lv[kBinWarps][VPL][32];     // per lane, view u: mx, my, first, items before u
-  __shared__ float4 s_gv[kBinWarps][32][2];       // per group: ellipse constants, rmin
+  __shared__ unsigned long long s_mask[kBW][32][kSlotRows];  // [warp][group][row]
+  __shared__ int s_flag[kBW][32];
+  __shared__ int s_src[kBW][32];
+  __shared__ int s_seg[kBW][32];            // per lane: first item of its segment
+  __shared__ float4 s_lv[kBW][VPL][32];     // per lane, view u: mx, my, first, items before u
+  __shared__ float4 s_gv[kBW][32][2];       // per group: ellipse constants, rmin
   stage_cams(s_cam);
   __syncthreads();
   constexpr int GPW = 32 / G;
   const int s = c_fp.s, N = c_fp.N, TX = c_fp.TX, TY = c_fp.TY;
   const int lane = threadIdx.x & 31, v = lane & (G - 1), gi = lane / G, w = threadIdx.x >> 5;
   const bool lead = v == 0;
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBinWarps;
-  for (unsigned long long wb = (blockIdx.x * (unsigned long long)kBinThreads + threadIdx.x) / 32 * GPW;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kBW;
+  for (unsigned long long wb = (blockIdx.x * (unsigned long long)NTH + threadIdx.x) / 32 * GPW;
        wb < n; wb += nwarps * GPW) {  // warp-uniform loop
     const unsigned long long g = wb + gi;
     const bool active = g < n;
