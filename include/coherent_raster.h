@@ -141,8 +141,10 @@ cr_status cr_make_orbit_rig(const cr_display* display, const float look_at[3], c
  * Options:
  *   cluster_size   s = |V_k| (1..32; default 8); s = 1 is "w/o reuse"
  *   remap          1 = View-coherent Remapping (default), 0 = raster order
- *   kernel         0 = B200 staged composite (warp per cluster chunk, shared
- *                  memory batches, ballot early exit) [requires remap = 1];
+ *   kernel         0 = B200 staged composite (warp per cluster chunk of up to
+ *                  32 lanes x two subpixels of one view, shared-memory
+ *                  batches, per-view cull ballots, early exit) [requires
+ *                  remap = 1];
  *                  1 = thread-per-subpixel composite (the paper's design,
  *                  Alg.2 Alpha-Blend), used for remap = 0 and for ablations
  *   background     colour added with the remaining transmittance (Z18)

@@ -1,5 +1,5 @@
-O=gpurun_out/s3ab; mkdir -p $O
-timeout 600 python tools/exp_equal.py C 0 4096 > $O/equal.txt 2>&1
-timeout 900 python tools/ab_exp.py C 0,4096 > $O/abC.txt 2>&1
-timeout 600 python tools/ab_exp.py B 0,4096 > $O/abB.txt 2>&1
+O=gpurun_out/s3ad; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 900 python bench.py > $O/bench_configC.json 2> $O/bench_configC.err
 echo done
