@@ -234,6 +234,24 @@ T* P_(DevBuf& b) { return (T*)b.p; }
 
 unsigned grid_for(long long n, int block) { return (unsigned)((n + block - 1) / block); }
 
+// Kernels whose cameras are staged in dynamic shared memory (N x 80 B, up to
+// 20 KB at N = 255) on top of their static arrays: allow the opt-in maximum
+// of dynamic shared memory per block once per kernel (the default caps static
+// + dynamic at 48 KB).
+template <auto kernel>  // one instantiation (and one flag) per kernel
+void allow_dyn_smem() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && optin > (int)fa.sharedSizeBytes)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+  done = true;
+}
+
 // device exclusive scan: out(i, excl, in(i)); *d_total = sum
 template <class In, class Out>
 cr_status dev_scan(cr_ctx* c, In in, Out out, long long n, uint32_t* d_total) {
@@ -1027,9 +1045,12 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     const unsigned count_grid =
         (unsigned)std::min<long long>(148 * 64, std::max<long long>(148, ((long long)nvis + 63) / 64));
 #define CR_COUNTL(GL, VL)                                                                      \
-  k_countv<GL, VL><<<count_grid, kBinThreads, cam_smem, str>>>(                                 \
-      rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),        \
-      P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6)
+  do {                                                                                          \
+    allow_dyn_smem<k_countv<GL, VL>>();                                                         \
+    k_countv<GL, VL><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
+        rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),      \
+        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                                 \
+  } while (0)
   // lanes per record x views per lane (measured at C, s = 8: 4 x 2 -> 2 x 4 lanes/views
   // took binning 5.65 -> 5.28 ms, s = 4: 4 x 1 -> 2 x 2 7.29 -> 6.21 ms, s = 2: 2 x 1 ->
   // 1 x 2 9.46 -> 8.70 ms; P2K s = 16:
@@ -1042,6 +1063,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   else if (GG >= 8) CR_COUNTL((GG >= 8 ? GG / 2 : 1), 2);                                     \
   else CR_COUNTL(GG, 1);                                                                      \
   CR_LAUNCHED(c);                                                                             \
+  allow_dyn_smem<k_count_big<GG>>();                                                          \
   k_count_big<GG><<<bin_grid, kBinThreads, cam_smem, str>>>(                                   \
       P_<uint32_t>(c->biglist), rec_sorted, sc + 6, P_<float4>(c->mean4), P_<float4>(c->geom), \
       P_<uint32_t>(c->cnt), bigrows)
@@ -1092,6 +1114,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     };
     auto launch_big = [&]() {
 #define CR_EMITB(GG)                                                                        \
+  allow_dyn_smem<k_emit_big<GG>>();                                                          \
   k_emit_big<GG><<<bin_grid, kBinThreads, cam_smem, c->side>>>(                              \
       rec_sorted, P_<uint32_t>(c->offs), P_<uint32_t>(c->biglist), sc + 6, P_<float4>(c->mean4), \
       P_<float4>(c->geom), tA, pA, bigrows)

@@ -17,11 +17,13 @@ from test_gpu_parity import _need_gpu, check_frame, make_pair
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("s", [1, 2])
+@pytest.mark.parametrize("s", [1, 2, 4, 8, 16, 24, 32])
 def test_max_views_255(s):
     # P:246 N views; the ABI's maximum N = 255 (u8 view map).  At s=1 every
     # view is its own cluster (K = 255, Bit_K = 8): a 16x16 tile holds up to
-    # K + 24 cluster-aligned chunks, far beyond round 1's 128-chunk cap.
+    # K + 24 cluster-aligned chunks, far beyond round 1's 128-chunk cap.  Every
+    # count lane/view split runs with 255 cameras (20 KB) in dynamic shared
+    # memory on top of its static arrays (past the default 48 KB per block).
     _need_gpu()
     W, H, N = 256, 144, 255
     sc = sy.random_scene(1500, 1, seed=41, scale_median=0.04)

@@ -1,5 +1,4 @@
-O=gpurun_out/s3ad; mkdir -p $O
+O=gpurun_out/s3af; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
-timeout 900 python bench.py > $O/bench_configC.json 2> $O/bench_configC.err
+timeout 600 python tools/ab_time.py C 15 > $O/abC.txt 2>&1
 echo done
