@@ -1056,12 +1056,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   // 1 x 2 9.46 -> 8.70 ms; P2K s = 16:
   // 4 x 4 no faster than 8 x 2; P4K s = 18: 8 x 3 instead of 16 x 2, 9.2 -> 8.3 ms)
 #define CR_COUNTS(GG)                                                                         \
-  if (GG == 32 && s <= 24 && (c->exp & 4096)) {                                              \
-    allow_dyn_smem<k_countv<4, 6, 128>>();                                                    \
-    k_countv<4, 6, 128><<<count_grid * 2, 128, cam_smem, str>>>(                              \
-        rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),    \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                               \
-  } else if (GG == 32 && s <= 24) CR_COUNTL(8, 3);                                            \
+  if (GG == 32 && s <= 24) CR_COUNTL(8, 3);                                                   \
   else if (GG == 8) CR_COUNTL(2, 4);                                                          \
   else if (GG == 4) CR_COUNTL(2, 2);                                                          \
   else if (GG == 2) CR_COUNTL(1, 2);                                                          \
