@@ -115,7 +115,7 @@ struct cr_ctx {
   std::vector<CamConstDev> ccon;
   float znear = 0.01f;
   // frame buffers
-  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, slots, biglist;
+  DevBuf rec0, rec1, geom, vis, cnt, dkey, offs, slots, rows8, biglist;
   DevBuf bigcnt, bigmask, bigwlo, biginfo;  // union rows of big records (k_count_big)
   DevBuf ka, va, kb, vb;           // record sort ping-pong
   DevBuf pta, pva, ptb, pvb;       // pair sort ping-pong
@@ -482,7 +482,7 @@ void cr_destroy(cr_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* all[] = {&c->mean4, &c->cov8, &c->shsoa, &c->V, &c->psi, &c->chunks, &c->nchunks, &c->psi2,
-                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->biglist, &c->bigcnt,
+                   &c->rec0, &c->rec1, &c->geom, &c->vis, &c->slots, &c->rows8, &c->biglist, &c->bigcnt,
                    &c->bigmask, &c->bigwlo, &c->biginfo, &c->cnt, &c->dkey, &c->offs, &c->ka, &c->va, &c->kb,
                    &c->vb, &c->pta, &c->pva, &c->ptb, &c->pvb, &c->hist, &c->look, &c->slook,
                    &c->scalars, &c->S, &c->E, &c->stage_out, &c->frames, &c->tmp};
@@ -961,6 +961,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
   CR_TRY(ensure(c, c->vb, Rz * 4));
   CR_TRY(ensure(c, c->offs, Rz * 4));
   CR_TRY(ensure(c, c->slots, Rz * 64));
+  CR_TRY(ensure(c, c->rows8, Rz));
   CR_TRY(ensure(c, c->biglist, Rz * 4));
   // stored union rows for up to 1/64 of the records (0.66 % are big at config C)
   const size_t bcap = std::max<size_t>(4096, Rz / 64);
@@ -1049,7 +1050,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
     allow_dyn_smem<k_countv<GL, VL>>();                                                         \
     k_countv<GL, VL><<<count_grid, kBinThreads, cam_smem, str>>>(                               \
         rec_sorted, nvis, P_<float4>(c->mean4), P_<float4>(c->geom), P_<uint32_t>(c->cnt),      \
-        P_<uint4>(c->slots), P_<uint32_t>(c->biglist), sc + 6);                                 \
+        P_<uint4>(c->slots), P_<uint8_t>(c->rows8), P_<uint32_t>(c->biglist), sc + 6);          \
   } while (0)
   // lanes per record x views per lane (measured at C, s = 8: 4 x 2 -> 2 x 4 lanes/views
   // took binning 5.65 -> 5.28 ms, s = 4: 4 x 1 -> 2 x 2 7.29 -> 6.21 ms, s = 2: 2 x 1 ->
@@ -1110,7 +1111,7 @@ cr_status cr_render_interlaced(cr_ctx* c, const cr_render_opts* o, void* out, si
       // 5.94 ms; P4K unchanged)
       cudaFuncSetAttribute(k_emit_rows<kWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       k_emit_rows<kWB, true><<<eg, 256, sm, str>>>(rec_sorted, P_<uint32_t>(c->offs), nvis, P,
-                                                   P_<uint4>(c->slots), tA, pA);
+                                                   P_<uint4>(c->slots), P_<uint8_t>(c->rows8), tA, pA);
     };
     auto launch_big = [&]() {
 #define CR_EMITB(GG)                                                                        \

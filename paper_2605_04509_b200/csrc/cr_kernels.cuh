@@ -687,6 +687,7 @@ __global__ void __launch_bounds__(NTH) k_countv(const uint32_t* __restrict__ rec
                                                         const float4* __restrict__ geom,
                                                         uint32_t* __restrict__ cnt,
                                                         uint4* __restrict__ slots,
+                                                        uint8_t* __restrict__ rows8,
                                                         uint32_t* __restrict__ big,
                                                         uint32_t* __restrict__ n_big) {
   constexpr int kBW = NTH / 32;  // warps per block
@@ -838,7 +839,8 @@ __global__ void __launch_bounds__(NTH) k_countv(const uint32_t* __restrict__ rec
 #pragma unroll
       for (int q = 1; q < G; q <<= 1) pc += __shfl_xor_sync(0xffffffffu, pc, q);
       if (wr) c = pc;
-      for (int q = v; wr && q < 4; q += G) {
+      // masks of rows >= nrows are never read (k_emit_rows loads by rows8)
+      for (int q = v; wr && q < 4 && 2 * q - 1 <= nrows; q += G) {
         uint4 val;
         if (q == 0) {
           val = make_uint4((uint32_t)(rmin & 0xFFFF) | ((uint32_t)nrows << 16), (uint32_t)lo_ref, c, 0u);
@@ -852,7 +854,10 @@ __global__ void __launch_bounds__(NTH) k_countv(const uint32_t* __restrict__ rec
       slots[4ull * o] = make_uint4(kSlotOverflow, 0u, 0u, 0u);
       big[atomicAdd(n_big, 1u)] = (uint32_t)o;
     }
-    if (active && lead) cnt[o] = c;
+    if (active && lead) {
+      cnt[o] = c;
+      rows8[o] = (uint8_t)(slow ? 7 : (fast ? nrows : 0));  // 7: overflow (header only)
+    }
     __syncwarp();
   }
 }
@@ -875,14 +880,16 @@ __global__ void __launch_bounds__(NTH) k_countv(const uint32_t* __restrict__ rec
 // Per-block inputs of the emission: the records' output offsets, the slot
 // (header + six row masks) and payload r of lane e = b*32 + lane.
 struct EmitIn {
-  uint32_t o, f1, r;
+  uint32_t o, f1, r, rows;
   uint4 h, s1, s2, s3;
 };
-__device__ __forceinline__ void emit_load_offs(const uint32_t* __restrict__ offs, uint32_t n,
+__device__ __forceinline__ void emit_load_offs(const uint32_t* __restrict__ offs,
+                                               const uint8_t* __restrict__ rows8, uint32_t n,
                                                uint32_t P, uint32_t nblk, uint32_t b, int lane,
                                                EmitIn& in) {
   const uint32_t e = b * 32u + (uint32_t)lane;
   in.o = (b < nblk && e < n) ? offs[e] : P;
+  in.rows = (b < nblk && e < n) ? rows8[e] : 0u;
   in.f1 = (b < nblk && b * 32u + 32u < n) ? offs[b * 32u + 32u] : P;
 }
 __device__ __forceinline__ void emit_load_slots(const uint32_t* __restrict__ rec_sorted,
@@ -898,11 +905,12 @@ __device__ __forceinline__ void emit_load_slots(const uint32_t* __restrict__ rec
   in.s3 = in.s1;
   in.r = ok ? rec_sorted[e] : 0u;
   if (ok && o1 > in.o) {  // the slot of a record without tiles is never written
+    // only the masks of the record's rows (rows8: 1..6, 7 = overflow, header only)
     const uint4* sl = slots + 4ull * e;
     in.h = sl[0];
-    in.s1 = sl[1];
-    in.s2 = sl[2];
-    in.s3 = sl[3];
+    if (in.rows != 7u) in.s1 = sl[1];
+    if (in.rows > 2u && in.rows != 7u) in.s2 = sl[2];
+    if (in.rows > 4u && in.rows != 7u) in.s3 = sl[3];
   }
 }
 
@@ -912,6 +920,7 @@ template <int WB, bool PF = false>
 __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ rec_sorted,
                                                    const uint32_t* __restrict__ offs, uint32_t n,
                                                    uint32_t P, const uint4* __restrict__ slots,
+                                                   const uint8_t* __restrict__ rows8,
                                                    uint32_t* __restrict__ out_t,
                                                    uint32_t* __restrict__ out_v) {
   extern __shared__ uint32_t s_obuf[];  // WB > 0: [8 warps][2][WB] staged (tile, payload)
@@ -932,9 +941,9 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
   EmitIn cur, nx;
   if (PF) {
     const uint32_t b0 = blockIdx.x * 8u + (uint32_t)w;
-    emit_load_offs(offs, n, P, nblk, b0, lane, cur);
+    emit_load_offs(offs, rows8, n, P, nblk, b0, lane, cur);
     emit_load_slots(rec_sorted, slots, n, nblk, b0, lane, cur);
-    emit_load_offs(offs, n, P, nblk, b0 + bstep, lane, nx);
+    emit_load_offs(offs, rows8, n, P, nblk, b0 + bstep, lane, nx);
   }
   for (uint32_t b = blockIdx.x * 8u + (uint32_t)w; b < nblk; b += bstep) {
     const uint32_t e = b * 32u + (uint32_t)lane;
@@ -942,11 +951,11 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
     if (PF) {  // issue the next block's slots and the offsets after it
       emit_load_slots(rec_sorted, slots, n, nblk, b + bstep, lane, nx);
     } else {
-      emit_load_offs(offs, n, P, nblk, b, lane, cur);
+      emit_load_offs(offs, rows8, n, P, nblk, b, lane, cur);
       emit_load_slots(rec_sorted, slots, n, nblk, b, lane, cur);
     }
     EmitIn nn;
-    if (PF) emit_load_offs(offs, n, P, nblk, b + 2 * bstep, lane, nn);
+    if (PF) emit_load_offs(offs, rows8, n, P, nblk, b + 2 * bstep, lane, nn);
     const uint32_t o = cur.o, f1 = cur.f1;
     const uint4 h = cur.h, s1 = cur.s1, s2 = cur.s2, s3 = cur.s3;
     const bool dec = !(h.x & kSlotOverflow);  // fast record (big ones: k_emit_big)
@@ -1036,6 +1045,7 @@ __global__ void __launch_bounds__(256) k_emit_rows(const uint32_t* __restrict__ 
       cur = nx;
       nx.o = nn.o;
       nx.f1 = nn.f1;
+      nx.rows = nn.rows;
     }
   }
 }
