@@ -586,7 +586,9 @@ __global__ void __launch_bounds__(128) k_preprocess(
           geom[2 * r] = make_float4(el.ex, el.ey, el.dyR, el.tc);
           geom[2 * r + 1] = make_float4(el.ic, el.b, el.det, 0.0f);
         }
-        const float A = c / det, B = -b / det, C = a / det;  // conic (tolerance path)
+        // conic (tolerance path): one correctly rounded reciprocal of det, three products
+        const float idet = __frcp_rn(det);
+        const float A = c * idet, B = -b * idet, C = a * idet;
         rec0[2 * r] = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, lo2);
         // SH colour at the representative camera centre (O11)
         const CamConstDev& cc = c_ccon[jr];
